@@ -1,0 +1,503 @@
+#!/usr/bin/env python
+"""TSQBX near-field benchmark (BASELINE.json metric: source-target pair-evals/s, fp64,
+and % of the FP64 roofline).
+
+Default: N=1, configuration 2 of BASELINE.json (Laplace TSQBX, p=8, N=262,144
+Fibonacci-sphere sources, 2 targets per center), `dense` near preset (16r, the
+stated mean ~200 sources per center).  One "step" = one
+evaluation of every (center, target) of that problem.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) centers are sharded by pair count across ranks, sources
+are replicated, and each step ends with one NCCL all-gather of the per-target
+potentials (strong scaling: the problem is fixed).  `--impl reference` times
+the reference's own compiled CPU core (oracle/_ref, built from /root/reference)
+on the host's cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "TSQBX source-target pair-evals/sec (fp64)"
+UNIT = "pair-evals/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--case", default="c2")
+    ap.add_argument("--preset", default="dense", choices=("dense", "literal"))
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--soak-seconds", type=float, default=1.0)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--group-lanes", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload_name(case) -> str:
+    d = case.describe()
+    eq = "Laplace" if d["equation"] == "laplace" else f"Helmholtz k={d['k']:g}"
+    return (f"BASELINE config {case.name[1]}: {eq} TSQBX S p={d['p']}, {d['n_sources']} sources, "
+            f"{d['n_centers']} centers, {d['n_targets']} targets, near radius "
+            f"{d['near_mult']:g}r ({case.preset})")
+
+
+# ----------------------------------------------------------------------------- clocks
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    """Polls SM clock, utilisation and throttle reasons (NVML) every 50 ms."""
+
+    def __init__(self, index: int):
+        self.samples = []
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, util, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.th.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": self.err}
+        loaded = [s for s in self.samples if s[1] >= 50] or self.samples
+        reasons = set()
+        for _, _, rs in loaded:
+            for bit, name in _REASONS.items():
+                if rs & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in loaded) if loaded else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(loaded)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def fp64_peak_tflops(torch, dev):
+    """DFMA throughput of this GPU (MEASURED_PEAKS.json has no FP64 entry)."""
+    from paper_1811_01110_b200 import _lib
+    L = _lib.load()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks, threads, iters = sms * 8, 256, 1 << 15
+    buf = torch.empty(blocks * threads, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    best = 0.0
+    for i in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.tsqbx_fp64_probe(buf.data_ptr(), iters, blocks, threads, st), "fp64 probe")
+        e1.record()
+        e1.synchronize()
+        if i >= 1:
+            best = max(best, blocks * threads * iters * 16 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def time_device_steps(torch, fn, steps, flush_buf):
+    """Per-step device time (CUDA events on the launching stream) with an L2 flush
+    (write of a 256 MB buffer) between steps, outside the events."""
+    ms = []
+    for _ in range(steps):
+        flush_buf.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        ms.append((e0, e1))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ms]
+
+
+def load_traffic(key):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(key)
+    except (OSError, ValueError):
+        return None
+
+
+def sample_centers(case, n, seed=123):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(case.n_centers, size=min(n, case.n_centers), replace=False))
+
+
+def cpu_sample_problem(case, sel):
+    """CPU near lists for a subset of centers (oracle membership builder) + their targets."""
+    import oracle
+    ptr, idx = oracle.near_csr(case.centers[sel], case.near_radii[sel], case.sources)
+    ntg = np.diff(case.tgt_ptr)[sel]
+    tptr = np.concatenate([[0], np.cumsum(ntg)])
+    tsel = np.concatenate([np.arange(case.tgt_ptr[c], case.tgt_ptr[c + 1]) for c in sel])
+    return ptr, idx, tptr, tsel
+
+
+def run_reference_chunk(args_tuple):
+    """Worker: the reference's compiled core over centers [lo, hi) of the sample."""
+    import oracle
+    lo, hi = args_tuple
+    S = _REF_STATE
+    core = oracle.ref_core()
+    case = S["case"]
+    ptr, idx, tptr, tsel = S["ptr"], S["idx"], S["tptr"], S["tsel"]
+    sub_ptr = ptr[lo:hi + 1] - ptr[lo]
+    sub_idx = idx[ptr[lo]:ptr[hi]]
+    sub_tptr = tptr[lo:hi + 1] - tptr[lo]
+    spec = case.cfg.spec
+    oracle.ref_ts_batch(core, "laplace" if spec.is_laplace else "helmholtz", spec.variant_code,
+                        spec.helmholtz_k or 0.0, case.cfg.p_qbx, case.sources, case.weights,
+                        case.centers[S["sel"][lo:hi]], sub_ptr, sub_idx,
+                        case.targets[tsel[tptr[lo]:tptr[hi]]], sub_tptr)
+    return int(np.sum(np.diff(sub_ptr) * np.diff(sub_tptr)))
+
+
+_REF_STATE = {}
+
+
+def cpu_reference_rate(case, seconds, processes=1, n_sample=200000):
+    """Reference compiled core (oracle/_ref) on a bounded sample of the workload:
+    returns (pairs/s, cores, kind, sample description)."""
+    import oracle
+    core = oracle.ref_core()
+    kind = "reference" if core is not None else "port"
+    if _REF_STATE.get("key") != (id(case), n_sample):
+        sel = sample_centers(case, n_sample)
+        ptr, idx, tptr, tsel = cpu_sample_problem(case, sel)
+        _REF_STATE.update(key=(id(case), n_sample), case=case, sel=sel, ptr=ptr, idx=idx,
+                          tptr=tptr, tsel=tsel)
+    sel, ptr, idx, tptr, tsel = (_REF_STATE[k] for k in ("sel", "ptr", "idx", "tptr", "tsel"))
+    chunk = 256
+    spec = case.cfg.spec
+    if core is None:
+        t0 = time.perf_counter()
+        pairs, lo = 0, 0
+        while time.perf_counter() - t0 < seconds and lo < len(sel):
+            hi = min(lo + chunk, len(sel))
+            sp = ptr[lo:hi + 1] - ptr[lo]
+            st = tptr[lo:hi + 1] - tptr[lo]
+            oracle.ts_batch("laplace" if spec.is_laplace else "helmholtz", 0,
+                            spec.helmholtz_k or 0.0, case.cfg.p_qbx, case.sources, case.weights,
+                            case.centers[sel[lo:hi]], sp, idx[ptr[lo]:ptr[hi]],
+                            case.targets[tsel[tptr[lo]:tptr[hi]]], st, nthreads=processes)
+            pairs += int(np.sum(np.diff(sp) * np.diff(st)))
+            lo = hi
+        dt = time.perf_counter() - t0
+        return pairs / dt, processes, kind, f"{lo} seeded-random centers, {pairs} pairs, {dt:.1f} s"
+    if processes == 1:
+        t0 = time.perf_counter()
+        pairs, lo = 0, 0
+        while time.perf_counter() - t0 < seconds and lo < len(sel):
+            hi = min(lo + chunk, len(sel))
+            pairs += run_reference_chunk((lo, hi))
+            lo = hi
+        dt = time.perf_counter() - t0
+        return (pairs / dt, 1, kind,
+                f"{lo} seeded-random centers of {case.n_centers} ({pairs} pairs), driver-style "
+                f"_core.ts_accum_* per (center, target), 1 process, {dt:.1f} s")
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(processes) as pool:
+        # calibrate: one chunk per worker
+        t0 = time.perf_counter()
+        pairs = sum(pool.map(run_reference_chunk, [(i * chunk, (i + 1) * chunk)
+                                                    for i in range(processes)]))
+        rate0 = pairs / (time.perf_counter() - t0)
+        per_center = pairs / (processes * chunk)
+        n = int(min(len(sel), max(processes * chunk, rate0 * seconds / per_center)))
+        bounds = np.linspace(0, n, processes * 8 + 1).astype(int)
+        t0 = time.perf_counter()
+        pairs = sum(pool.map(run_reference_chunk, list(zip(bounds[:-1], bounds[1:]))))
+        dt = time.perf_counter() - t0
+    return (pairs / dt, processes, kind,
+            f"{n} seeded-random centers of {case.n_centers} ({pairs} pairs), driver-style "
+            f"_core.ts_accum_* per (center, target), {processes} processes, {dt:.1f} s")
+
+
+# ----------------------------------------------------------------------------- reference arm
+def main_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1811_01110_b200 import configs
+    case = configs.make_case(args.case, args.preset)
+    procs = os.cpu_count() or 1
+    n_sample = case.n_centers if case.n_centers <= 300000 else 300000
+    step_seconds = max(1.0, min(6.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):      # warm-up (the first also builds the sample problem)
+        cpu_reference_rate(case, min(step_seconds, 1.0), processes=procs, n_sample=n_sample)
+    rates = []
+    for _ in range(args.steps):
+        rate, cores, kind, sample = cpu_reference_rate(case, step_seconds, processes=procs,
+                                                       n_sample=n_sample)
+        rates.append(rate)
+    value = float(statistics.median(rates))
+    cpu = {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+           "sample": sample + f"; median of {args.steps} steps"}
+    pairs_full = None
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_seconds * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json configuration geometry)",
+            "impl": "reference",
+            "config": {"workload": workload_name(case), "case": case.name,
+                       "preset": case.preset, "full_pairs_per_step": pairs_full},
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
+    """Device-resident kernel throughput for one case."""
+    from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    near = build_near_lists(case.centers, case.sources, case.near_radii, dev)
+    e1.record()
+    torch.cuda.synchronize()
+    csr_ms = e0.elapsed_time(e1)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev)
+    pairs = prob.pair_count()
+    for _ in range(max(3, args.warmup)):
+        prob.evaluate()
+    torch.cuda.synchronize()
+    clocks = None
+    if want_clocks:
+        sampler = ClockSampler(index)
+        with sampler:
+            t_end = time.perf_counter() + args.soak_seconds
+            while time.perf_counter() < t_end:     # soak: clocks settle under this load
+                for _ in range(20):
+                    prob.evaluate()
+                torch.cuda.synchronize()
+            ms = time_device_steps(torch, prob.evaluate, args.steps, flush)
+        clocks = sampler.summary()
+    else:
+        ms = time_device_steps(torch, prob.evaluate, args.steps, flush)
+    spec = case.cfg.spec
+    fpp = configs.algorithmic_flops_per_pair(spec, case.cfg.p_qbx)
+    mean_ms = sum(ms) / len(ms)
+    launches_per_step = 1 if spec.is_laplace else 2
+    res = {"pairs_per_step": pairs, "ms": ms, "mean_ms": mean_ms,
+           "value": pairs * len(ms) / (sum(ms) * 1e-3), "flops_per_pair": fpp,
+           "tflops": pairs * fpp / (mean_ms * 1e-3) / 1e12, "csr_build_ms": csr_ms,
+           "group_lanes": prob.group_lanes, "launches_per_step": launches_per_step,
+           "mean_list_len": near.mean_len}
+    return res, prob, clocks
+
+
+def measure_e2e(torch, case, args, dev):
+    """Through the public API with host (pinned) buffers: H2D of the geometry,
+    device near lists, TSQBX, D2H of the potentials -- every step."""
+    from paper_1811_01110_b200.tsqbx import near_field_potentials
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    src, w = pin(case.sources), pin(case.weights)
+    ctr, rad, tgt, tptr = pin(case.centers), pin(case.near_radii), pin(case.targets), \
+        pin(case.tgt_ptr)
+    h2d = sum(int(t.numel() * t.element_size()) for t in (src, w, ctr, rad, tgt, tptr))
+    d2h = case.n_targets * 16 + 16
+    fn = lambda: near_field_potentials(case.cfg, src, w, ctr, rad, tgt, tgt_ptr=tptr,  # noqa
+                                       validate=True, group_lanes=args.group_lanes or None,
+                                       device=dev)
+    for _ in range(max(1, min(args.warmup, 3))):
+        fn()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    ms = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    return {"ms": ms, "h2d": h2d, "d2h": d2h, "steps": steps}
+
+
+def main_ours(args):
+    import torch
+    from paper_1811_01110_b200 import configs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        return 1
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    case = configs.make_case(args.case, args.preset)
+    if world > 1:
+        return main_distributed(torch, args, case, dev, flush, rank, world, local)
+
+    peak = fp64_peak_tflops(torch, dev)
+    res, prob, clocks = measure_case(torch, case, args, dev, flush, want_clocks=True,
+                                     index=local)
+    frac = res["tflops"] / peak if peak else None
+    key = f"{case.name}/{case.preset}"
+    traffic = load_traffic(key)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["mean_ms"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Fibonacci sphere etc., BASELINE.json geometry; inputs "
+                "resident in HBM for `value`)",
+        "config": {"workload": workload_name(case), "case": case.name, "preset": case.preset,
+                   "pairs_per_step": res["pairs_per_step"],
+                   "mean_near_list": round(res["mean_list_len"], 2),
+                   "targets": case.n_targets, "group_lanes": res["group_lanes"],
+                   "l2": "flushed between steps (256 MB write, outside the timed events)",
+                   "csr_build_ms": round(res["csr_build_ms"], 3), "seed": case.seed,
+                   "validation": "off in `value` (driver path), on in `e2e` (public API)"},
+        "roofline": {"bound": "fp64", "achieved": res["tflops"], "peak": peak,
+                     "unit": "TFLOP/s", "frac": frac,
+                     "traffic": traffic,
+                     "peak_source": "measured DFMA probe on this GPU (tsqbx_fp64_probe); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "flops_per_pair": res["flops_per_pair"],
+                     "flops_convention": "algorithmic, SURVEY.md 8(d): Laplace 7p+17, "
+                                         "Helmholtz 14p+30 per pair"},
+        "gpu_launches": res["launches_per_step"] * args.steps,
+        "clocks": clocks,
+    }
+    if not args.no_e2e:
+        e2e = measure_e2e(torch, case, args, dev)
+        mean = sum(e2e["ms"]) / len(e2e["ms"])
+        line["e2e"] = {"value": res["pairs_per_step"] / (mean * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                       "ms_per_step": mean,
+                       "path": "paper_1811_01110_b200.tsqbx.near_field_potentials: pinned "
+                               "host arrays -> H2D -> device near lists -> TSQBX (validated) "
+                               "-> D2H"}
+    if not args.no_cpu_baseline:
+        rate, cores, kind, sample = cpu_reference_rate(case, args.cpu_seconds, processes=1)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": sample}
+    if not args.no_secondary:
+        sec = {}
+        del prob
+        for name, preset in (("c2", "literal" if case.preset == "dense" else "dense"),
+                             ("c3", "dense"), ("c3", "literal")):
+            if name == case.name and preset == case.preset:
+                continue
+            c2 = configs.make_case(name, preset)
+            r, p2, _ = measure_case(torch, c2, args, dev, flush)
+            sec[f"{name}/{preset}"] = {
+                "value": r["value"], "pairs_per_step": r["pairs_per_step"],
+                "ms_per_step": r["mean_ms"], "tflops": r["tflops"],
+                "roofline_frac": r["tflops"] / peak if peak else None,
+                "group_lanes": r["group_lanes"], "csr_build_ms": round(r["csr_build_ms"], 3),
+                "mean_near_list": round(r["mean_list_len"], 2)}
+            del p2
+            torch.cuda.empty_cache()
+        line["secondary"] = sec
+    print(json.dumps(line))
+    return 0
+
+
+def main_distributed(torch, args, case, dev, flush, rank, world, local):
+    import torch.distributed as dist
+    from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs
+    from paper_1811_01110_b200.distributed import ShardedEvaluator
+
+    dist.init_process_group("nccl", device_id=dev)
+    near = build_near_lists(case.centers, case.sources, case.near_radii, dev)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev)
+    pairs = prob.pair_count()
+    sh = ShardedEvaluator(prob, rank, world)
+    for _ in range(max(3, args.warmup)):
+        sh.evaluate()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = time_device_steps(torch, sh.evaluate, args.steps, flush)
+    torch.cuda.synchronize()
+    dist.barrier()
+    total = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    t = float(total.item())
+    if rank == 0:
+        fpp = configs.algorithmic_flops_per_pair(case.cfg.spec, case.cfg.p_qbx)
+        line = {"metric": METRIC, "value": pairs * args.steps / (t * 1e-3), "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_name(case), "case": case.name,
+                           "preset": case.preset, "pairs_per_step": pairs,
+                           "parallelism": f"centers sharded by pair count over {world} ranks, "
+                                          "sources replicated, 1 NCCL all-gather per step"},
+                "roofline": {"bound": "fp64", "achieved": pairs * fpp / (t / args.steps * 1e-3)
+                             / 1e12 / world, "unit": "TFLOP/s per GPU", "peak": None,
+                             "frac": None, "traffic": None},
+                "gpu_launches": 2 * args.steps}
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return main_reference(args)
+    return main_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

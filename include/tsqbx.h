@@ -1,0 +1,198 @@
+/*
+ * include/tsqbx.h -- C ABI of the B200-native TSQBX near-field evaluator.
+ *
+ * Drop-in boundary for the reference's backend plugin protocol
+ * (/root/reference/pkg/src/gigaqbx/_backend/__init__.py:7-41): every backend
+ * module exposes
+ *     ts_accum_laplace(variant, p, sources, weights, snormals, center, target, tnormal)
+ *         -- _core.pyx:205-207, _backend/_ref.py:177, _backend/compiled.py:65-69
+ *     ts_accum_helmholtz(variant, k, p, sources, weights, snormals, center, target, tnormal)
+ *         -- _core.pyx:310-312, _backend/_ref.py:278, _backend/compiled.py:72-76
+ * for ONE (center, target) over a batch of sources.  This ABI is the batched
+ * form of the same call: many centers, each with a CSR row of near sources and
+ * a contiguous run of targets.  A call with n_ctr = 1 and n_tgt = 1 is exactly
+ * the reference function.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers, caller-owned; no hidden allocation.
+ *     Scratch is passed in as `workspace` (size from the *_workspace_bytes query).
+ *   - Complex numbers are interleaved (re, im) doubles (numpy complex128 layout).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All calls are
+ *     stream-ordered and asynchronous unless stated otherwise.
+ *   - Return value: TSQBX_OK or an error code; tsqbx_last_error() has the text.
+ *   - Variant codes follow _backend/common.py:27-29 (0 = S, 1 = S', 2 = D);
+ *     equations: 0 = Laplace, 1 = Helmholtz (kernels.py:26-28).
+ *   - Validation (flag TSQBX_FLAG_VALIDATE) mirrors tsqbx._prep (tsqbx.py:38-53):
+ *     a flagged problem leaves *err_key != INT64_MAX; tsqbx_validate() then
+ *     locates the first offending (target, list position) exactly.
+ */
+#ifndef GIGAQBX_B200_TSQBX_H
+#define GIGAQBX_B200_TSQBX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSQBX_ABI_VERSION 1
+
+#define TSQBX_OK 0
+#define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
+#define TSQBX_ERR_COINCIDENT 2   /* tsqbx.py:44-47  "source i coincides with the expansion center" */
+#define TSQBX_ERR_ARGUMENT 3
+#define TSQBX_ERR_CUDA 4
+
+#define TSQBX_EQ_LAPLACE 0
+#define TSQBX_EQ_HELMHOLTZ 1
+
+#define TSQBX_VARIANT_S 0
+#define TSQBX_VARIANT_SPRIME 1
+#define TSQBX_VARIANT_D 2
+
+#define TSQBX_FLAG_VALIDATE 1u   /* cheap in-kernel screening, see tsqbx_validate */
+#define TSQBX_FLAG_GENERIC 2u    /* force the runtime-p reference-order kernel */
+
+#define TSQBX_MAX_ORDER 64
+
+/* err_key encoding (int64, device scalar; INT64_MAX = no problem):
+ *   (target << 32) | (kind << 31) | list_position,  kind 0 = coincident, 1 = separation.
+ * After tsqbx_eval with TSQBX_FLAG_VALIDATE the key is only a screen
+ * (TSQBX_ERR_KEY_SUSPECT); tsqbx_validate produces the exact key. */
+#define TSQBX_ERR_KEY_NONE INT64_MAX
+#define TSQBX_ERR_KEY_SUSPECT (INT64_MAX - 1)
+
+int tsqbx_abi_version(void);
+const char* tsqbx_last_error(void);
+/* number of SMs and compute capability of the current device (host query) */
+int tsqbx_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------------------------------------
+ * Source packing.  The evaluator reads sources in a packed, 32-byte aligned
+ * layout: double4 {x, y, z, Re w} per source, then Im w per source, then (with
+ * normals) double4 {nx, ny, nz, 0}.  packed[i] = source perm[i] (perm may be NULL).
+ * ------------------------------------------------------------------------- */
+int64_t tsqbx_packed_doubles(int64_t n_src, int with_normals);
+int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const double* nrm,
+                       const int32_t* perm, double* packed, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Evaluation.  Every per-center array is in PROCESSING order (row g):
+ *   packed      : tsqbx_pack_sources output (n_src sources)
+ *   ctr_xyz     : n_ctr x 3 centers, row g
+ *   near_ptr    : n_ctr + 1 row offsets into near_idx
+ *   near_idx    : source indices into `packed`
+ *   tgt_xyz     : n_tgt x 3 targets grouped by row: the targets of row g are
+ *                 tgt_ptr[g] .. tgt_ptr[g+1]-1
+ *   tgt_nrm     : n_tgt x 3 (S' only, else NULL)
+ *   tgt_out     : output slot of each target (NULL = identity); the value of
+ *                 target t is written to out[(tgt_out ? tgt_out[t] : t) - out_offset]
+ *   out         : complex128 potentials
+ *   err_key     : device int64 (see above); may be NULL when flags lacks VALIDATE
+ * A user CSR (rows by user center) is already in processing order (identity);
+ * tsqbx_order_targets produces these arrays for a Morton order from
+ * tsqbx_near_count.  A contiguous row range [g0, g1) of a problem is evaluated
+ * by offsetting ctr_xyz / near_ptr / tgt_ptr by g0 (how ranks shard it).
+ * ------------------------------------------------------------------------- */
+int64_t tsqbx_eval_workspace_bytes(int equation, int variant, int p, int64_t n_tgt);
+int tsqbx_eval_packed(int equation, int variant, double k, int p,
+                      const double* packed, int64_t n_src, int with_normals,
+                      const double* ctr_xyz, int64_t n_ctr,
+                      const int64_t* near_ptr, const int32_t* near_idx,
+                      const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
+                      int64_t n_tgt, const int64_t* tgt_out, int64_t out_offset,
+                      unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
+                      double* out, int64_t* err_key, void* stream);
+
+/* Convenience forms with the reference's names: raw user-layout sources
+ * (xyz n x 3, complex weights, optional normals), user-order CSR.  They pack
+ * into `workspace` (size: tsqbx_user_workspace_bytes) and call tsqbx_eval_packed. */
+int64_t tsqbx_user_workspace_bytes(int equation, int variant, int p, int64_t n_src,
+                                   int64_t n_tgt);
+int tsqbx_eval_laplace(int variant, int p,
+                       const double* src_xyz, const double* src_w, const double* src_nrm,
+                       int64_t n_src, const double* ctr_xyz, int64_t n_ctr,
+                       const int64_t* near_ptr, const int32_t* near_idx,
+                       const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
+                       int64_t n_tgt, unsigned flags, void* workspace, int64_t ws_bytes,
+                       double* out, int64_t* err_key, void* stream);
+int tsqbx_eval_helmholtz(int variant, double k, int p,
+                         const double* src_xyz, const double* src_w, const double* src_nrm,
+                         int64_t n_src, const double* ctr_xyz, int64_t n_ctr,
+                         const int64_t* near_ptr, const int32_t* near_idx,
+                         const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
+                         int64_t n_tgt, unsigned flags, void* workspace, int64_t ws_bytes,
+                         double* out, int64_t* err_key, void* stream);
+
+/* Exact validation in the reference's arithmetic (tsqbx.py:43-53): for every
+ * (target, list position) computes R = |s - c|, r = |t - c| and writes into
+ * *err_key the smallest key of a coincident (R == 0) or separated
+ * (R * (1 + 1e-12) < r) pair; coincidence outranks separation within a target. */
+int tsqbx_validate(const double* packed, int64_t n_src,
+                   const double* ctr_xyz, int64_t n_ctr,
+                   const int64_t* near_ptr, const int32_t* near_idx,
+                   const double* tgt_xyz, const int64_t* tgt_ptr, int64_t n_tgt,
+                   int64_t* err_key, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Radius-ball near lists on the device (no reference function: the reference
+ * builds tree lists, driver.py:197-228 / ilists.py:93-218; BASELINE.json
+ * defines radius balls).  member(s, c) iff ((dx*dx + dy*dy) + dz*dz) <= rad*rad
+ * in round-to-nearest without contraction.
+ *
+ * Two phases sharing one caller-owned workspace:
+ *   tsqbx_near_count: Morton-sorts sources and centers, counts, scans.
+ *       Writes src_perm (sorted position -> user source), ctr_order
+ *       (processing position -> user center), near_ptr (n_ctr + 1, rows in
+ *       processing order) and *n_pairs (device int64).
+ *   tsqbx_near_fill : writes near_idx (n_pairs entries, indices into the
+ *       sorted source order, ascending within each row).
+ * ------------------------------------------------------------------------- */
+int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src);
+int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                     const double* src_xyz, int64_t n_src,
+                     void* workspace, int64_t ws_bytes,
+                     int32_t* src_perm, int32_t* ctr_order, int64_t* near_ptr,
+                     int64_t* n_pairs, void* stream);
+int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                    const double* src_xyz, int64_t n_src,
+                    void* workspace, int64_t ws_bytes,
+                    const int32_t* ctr_order, const int64_t* near_ptr,
+                    int32_t* near_idx, void* stream);
+
+/* Reorder centers and their targets into the processing order `ctr_order`
+ * (user center ctr_order[g] becomes row g): writes ctr_out (n_ctr x 3),
+ * tptr_out (n_ctr + 1), tgt_out / tnrm_out (n_tgt x 3; tnrm only if tgt_nrm)
+ * and tgt_index (processing target -> user target; pass it as tgt_out of the
+ * evaluation to write potentials in user order). */
+int64_t tsqbx_order_workspace_bytes(int64_t n_ctr);
+int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* ctr_xyz,
+                        const int64_t* tgt_ptr, const double* tgt_xyz, const double* tgt_nrm,
+                        int64_t n_tgt, void* workspace, int64_t ws_bytes,
+                        double* ctr_out, int64_t* tptr_out, double* tgt_out, double* tnrm_out,
+                        int64_t* tgt_index, void* stream);
+
+/* out[dest[i]] = src[i] for n complex128 values (dest NULL = copy); assembles
+ * all-gathered shards into user target order. */
+int tsqbx_scatter_c128(int64_t n, const int64_t* dest, const double* src, double* out,
+                       void* stream);
+
+/* ---------------------------------------------------------------------------
+ * FP64 roofline probe: every thread runs 8 independent DFMA chains of `iters`
+ * steps (16 * iters flops per thread); used by bench.py to measure the FP64
+ * peak of the box (MEASURED_PEAKS.json has none).  out needs blocks*threads
+ * doubles.
+ * ------------------------------------------------------------------------- */
+int tsqbx_fp64_probe(double* out, int64_t iters, int blocks, int threads, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU helper: after each rank evaluated its contiguous block of targets,
+ * one NCCL all-gather assembles every target's potential on every rank
+ * (implemented in Python over torch.distributed/NCCL; see
+ * paper_1811_01110_b200/distributed.py).  Nothing to export here.
+ * ------------------------------------------------------------------------- */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

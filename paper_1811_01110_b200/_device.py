@@ -1,0 +1,45 @@
+"""Device-buffer plumbing (PyTorch is used only for allocation and streams)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("TSQBX evaluation needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda",
+                                                                       torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise RuntimeError(f"device {dev} is not a CUDA device")
+    return dev
+
+
+def stream_handle(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def to_device(a, dtype: torch.dtype, dev: torch.device, shape=None) -> torch.Tensor:
+    """Contiguous device tensor of `dtype` (copies host arrays; no-op for matching tensors)."""
+    if isinstance(a, torch.Tensor):
+        t = a.to(device=dev, dtype=dtype)
+    else:
+        np_dtype = {torch.float64: np.float64, torch.int64: np.int64, torch.int32: np.int32,
+                    torch.complex128: np.complex128}[dtype]
+        arr = np.ascontiguousarray(np.asarray(a, dtype=np_dtype))
+        t = torch.from_numpy(arr).to(device=dev, non_blocking=False)
+    t = t.contiguous()
+    if shape is not None:
+        t = t.reshape(shape)
+    return t
+
+
+def complex_as_f64(w: torch.Tensor) -> torch.Tensor:
+    """complex128 (n,) tensor -> interleaved float64 (n, 2) view."""
+    return torch.view_as_real(w.contiguous())
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()

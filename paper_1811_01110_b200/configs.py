@@ -1,0 +1,167 @@
+"""The five BASELINE.json workloads as seeded synthetic problems.
+
+Every case is a cloud of sources y_j with outward normals n_j, one QBX
+center per source at c_j = y_j - r_j n_j (``place_qbx_centers`` with side -1),
+the on-surface target t = y_j (C2/C3 add one off-surface target per center)
+and a radius-ball near list of radius m * r_j.
+
+BASELINE.json is inconsistent about the near radius:
+the literal radii (3r / 4r) give ~7-12 sources per center while the text
+states a mean of ~200, which the same geometry reaches at 16r.  Both are
+available: ``preset="literal"`` (3r for C1/C4/C5, 4r for C2/C3) and
+``preset="dense"`` (16r; for C4 a global r = 0.5*sqrt(area/N), the only
+variant giving the stated ~30..~800 spread).  The choices SURVEY.md
+Appendix B leaves open are recorded in DESIGN.md.
+
+RNG (``np.random.default_rng(seed)``) draw order, fixed:
+  C1-C3:  w_lap = U(0.5, 1.5)^N, u_off = normal(N, 3), w_re = U(-1, 1)^N, w_im = U(-1, 1)^N
+  C4:     jitter (N, 2), w_lap
+  C5:     sphere placement, then per sphere w_re, w_im
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import geometry as geo
+from .kernels import Equation, KernelSpec
+from .tsqbx import TsConfig
+
+PRESETS = ("literal", "dense")
+
+
+@dataclass
+class TsqbxCase:
+    name: str
+    preset: str
+    seed: int
+    cfg: TsConfig
+    sources: np.ndarray        # (N, 3)
+    weights: np.ndarray        # (N,) complex128
+    normals: np.ndarray        # (N, 3)
+    centers: np.ndarray        # (C, 3)
+    expansion_radii: np.ndarray  # (C,) r_j
+    near_radii: np.ndarray     # (C,) m * r_j
+    targets: np.ndarray        # (T, 3) grouped by center
+    tgt_ptr: np.ndarray        # (C + 1,)
+    notes: dict = field(default_factory=dict)
+
+    @property
+    def n_sources(self) -> int:
+        return self.sources.shape[0]
+
+    @property
+    def n_centers(self) -> int:
+        return self.centers.shape[0]
+
+    @property
+    def n_targets(self) -> int:
+        return self.targets.shape[0]
+
+    def describe(self) -> dict:
+        spec = self.cfg.spec
+        return {"case": self.name, "preset": self.preset, "seed": self.seed,
+                "equation": spec.equation.value, "variant": spec.variant.value,
+                "k": spec.helmholtz_k, "p": self.cfg.p_qbx, "n_sources": self.n_sources,
+                "n_centers": self.n_centers, "n_targets": self.n_targets, **self.notes}
+
+
+def _sphere_case(name, n, p, spec, preset, seed, off_surface, helmholtz_weights, mult_literal):
+    rng = np.random.default_rng(seed)
+    y, nrm = geo.fibonacci_sphere(n)
+    h = math.sqrt(4.0 * math.pi / n)
+    r = 0.5 * h
+    w_lap = (4.0 * math.pi / n) * rng.uniform(0.5, 1.5, n)
+    u_off = rng.normal(size=(n, 3))
+    w_re = rng.uniform(-1.0, 1.0, n)
+    w_im = rng.uniform(-1.0, 1.0, n)
+    weights = ((4.0 * math.pi / n) * (w_re + 1j * w_im) if helmholtz_weights
+               else w_lap.astype(np.complex128))
+    disc = geo.point_cloud_discretization(y, nrm, np.full(n, 4.0 * math.pi / n), h)
+    cs = geo.place_qbx_centers(disc, -1, 0.5)
+    m = mult_literal if preset == "literal" else 16.0
+    if off_surface:
+        u = u_off / np.linalg.norm(u_off, axis=1)[:, None]
+        toff = cs.centers + 0.5 * r * u
+        targets = np.empty((2 * n, 3))
+        targets[0::2] = y
+        targets[1::2] = toff
+        tptr = np.arange(0, 2 * n + 1, 2, dtype=np.int64)
+    else:
+        targets = y.copy()
+        tptr = np.arange(n + 1, dtype=np.int64)
+    return TsqbxCase(name=name, preset=preset, seed=seed, cfg=TsConfig(spec, p), sources=y,
+                     weights=weights, normals=nrm, centers=cs.centers,
+                     expansion_radii=cs.radii, near_radii=m * cs.radii, targets=targets,
+                     tgt_ptr=tptr, notes={"near_mult": m, "h": h})
+
+
+def make_case(name: str, preset: str = "dense", seed: int = 0, n: int | None = None,
+              spheres: int | None = None) -> TsqbxCase:
+    """Build configuration ``name`` in {c1..c5}.  ``n`` (points per sphere / torus)
+    and ``spheres`` (C5) shrink a case for tests; defaults are BASELINE sizes."""
+    if preset not in PRESETS:
+        raise ValueError(f"preset must be one of {PRESETS}")
+    name = name.lower()
+    lap = KernelSpec()
+    if name == "c1":
+        return _sphere_case("c1", n or 4096, 4, lap, preset, seed, False, False, 3.0)
+    if name == "c2":
+        return _sphere_case("c2", n or 262144, 8, lap, preset, seed, True, False, 4.0)
+    if name == "c3":
+        spec = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=10.0)
+        return _sphere_case("c3", n or 262144, 8, spec, preset, seed, True, True, 4.0)
+    if name == "c4":
+        return _torus_case(n or 1048576, preset, seed)
+    if name == "c5":
+        return _spheres_case(n or 524288, spheres or 16, preset, seed)
+    raise ValueError(f"unknown case {name!r}")
+
+
+def _torus_case(n, preset, seed):
+    rng = np.random.default_rng(seed)
+    y, nrm, h_loc = geo.clustered_torus(n, rng)
+    area = 4.0 * math.pi ** 2 * 1.0 * 0.35
+    w = (area / n) * rng.uniform(0.5, 1.5, n)
+    if preset == "literal":
+        r, m = 0.5 * h_loc, 3.0                     # per-source r = half the local spacing
+    else:
+        r, m = np.full(n, 0.5 * math.sqrt(area / n)), 16.0   # global r: ~30..~800 per list
+    disc = geo.point_cloud_discretization(y, nrm, np.full(n, area / n), 2.0 * r)
+    cs = geo.place_qbx_centers(disc, -1, 0.5)
+    return TsqbxCase(name="c4", preset=preset, seed=seed, cfg=TsConfig(KernelSpec(), 12),
+                     sources=y, weights=w.astype(np.complex128), normals=nrm,
+                     centers=cs.centers, expansion_radii=cs.radii, near_radii=m * cs.radii,
+                     targets=y.copy(), tgt_ptr=np.arange(n + 1, dtype=np.int64),
+                     notes={"near_mult": m})
+
+
+def _spheres_case(n_per, count, preset, seed):
+    rng = np.random.default_rng(seed)
+    origins, radii = geo.pack_spheres(count, rng)
+    ys, ns, ws, rs = [], [], [], []
+    for o, R in zip(origins, radii):
+        y, nrm = geo.fibonacci_sphere(n_per, R, o)
+        a = 4.0 * math.pi * R * R / n_per
+        w = a * (rng.uniform(-1.0, 1.0, n_per) + 1j * rng.uniform(-1.0, 1.0, n_per))
+        ys.append(y)
+        ns.append(nrm)
+        ws.append(w)
+        rs.append(np.full(n_per, 0.5 * R * math.sqrt(4.0 * math.pi / n_per)))
+    y, nrm, w, r = (np.concatenate(v) for v in (ys, ns, ws, rs))
+    m = 3.0 if preset == "literal" else 16.0
+    centers = y - r[:, None] * nrm
+    spec = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=20.0)
+    N = y.shape[0]
+    return TsqbxCase(name="c5", preset=preset, seed=seed, cfg=TsConfig(spec, 10), sources=y,
+                     weights=w, normals=nrm, centers=centers, expansion_radii=r,
+                     near_radii=m * r, targets=y.copy(), tgt_ptr=np.arange(N + 1, dtype=np.int64),
+                     notes={"near_mult": m, "spheres": count})
+
+
+def algorithmic_flops_per_pair(spec: KernelSpec, p: int) -> int:
+    """Laplace S 7p + 17, Helmholtz S 14p + 30."""
+    return 7 * p + 17 if spec.is_laplace else 14 * p + 30

@@ -1,0 +1,767 @@
+// eval.cu -- sm_100a fp64 TSQBX evaluation kernels + their C ABI entry points.
+//
+// Hot path: for every center c and each of its targets t,
+//   Laplace   u(t) = 1/(4 pi)  sum_{s in near(c)} w_s sum_{n<=p} |t-c|^n/|s-c|^{n+1} P_n(cos g)
+//   Helmholtz u(t) = ik/(4 pi) sum_{s in near(c)} w_s sum_{n<=p} (2n+1) j_n(k|t-c|) h_n(k|s-c|) P_n(cos g)
+// (reference: _core.pyx:205-307 and :310-419).
+//
+// Work decomposition: a group of G lanes (G in {1,2,4,8,16,32}) owns one
+// center; its lanes stride over the center's CSR row, every lane evaluating
+// one source against ALL of the center's targets (the source-side work -- s-c,
+// 1/R, h_n(kR) -- is shared by the targets), then the group reduces with
+// warp shuffles.  Centers arrive in Morton order from the CSR builder, so the
+// groups of one CTA read overlapping source neighbourhoods out of L1.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace tsqbx {
+
+namespace {
+thread_local char g_err[512] = "";
+}
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return TSQBX_OK;
+  return set_error(TSQBX_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct EvalParams {
+  const double4* __restrict__ sp;    // {x, y, z, Re w}
+  const double* __restrict__ swi;    // Im w
+  const double4* __restrict__ snrm;  // {nx, ny, nz, 0} or null
+  const double* __restrict__ ctr;    // processing order
+  const int64_t* __restrict__ nptr;
+  const int32_t* __restrict__ nidx;
+  const double* __restrict__ tgt;
+  const double* __restrict__ tnrm;
+  const int64_t* __restrict__ tptr;  // rows in processing order
+  const int64_t* __restrict__ tout;  // processing target -> output slot (null = identity)
+  const double* __restrict__ ttab;   // Helmholtz per-target Bessel table
+  double2* __restrict__ out;
+  int64_t out_offset;
+  unsigned long long* err;
+  int64_t n_ctr;
+  int ttab_stride;
+  int p;
+  int variant;
+  int G;
+  int validate;
+  double k;
+};
+
+__device__ __forceinline__ int64_t out_slot(const EvalParams& a, int64_t t) {
+  return (a.tout ? a.tout[t] : t) - a.out_offset;
+}
+
+__device__ __forceinline__ void flag_suspect(unsigned long long* err) {
+  atomicMin(err, (unsigned long long)TSQBX_ERR_KEY_SUSPECT);
+}
+
+// ---------------------------------------------------------------------------
+// Laplace S, compile-time order P, NT targets per pass.
+// Per pair: s-c, R^2, 1/R shared by the targets; per target A = (s-c).(t-c)/R^2,
+// B = |t-c|^2/R^2 and the 3-op/order Clenshaw series (common.cuh).
+// ---------------------------------------------------------------------------
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
+  const int G = a.G;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g = gt / G;
+  if (g >= a.n_ctr) return;
+  const int lane = (int)(threadIdx.x & (unsigned)(G - 1));
+  const unsigned mask = group_mask(G);
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int64_t b = a.nptr[g], e = a.nptr[g + 1];
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      tx[q] = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    for (int64_t j = b + lane; j < e; j += G) {
+      const int s = __ldg(a.nidx + j);
+      const double4 q4 = ld256(a.sp + s);
+      const double wim = __ldg(a.swi + s);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt(R2);
+      const double iR2 = iR * iR;
+      const double wr = q4.w * iR, wi = wim * iR;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const double A = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR2;
+        const double B = r2[q] * iR2;
+        const double S = laplace_series<P>(A, B);
+        ar[q] = fma(S, wr, ar[q]);
+        ai[q] = fma(S, wi, ai[q]);
+        if (VAL) bm[q] = fmax(bm[q], B);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      ar[q] = group_sum(ar[q], G, mask);
+      ai[q] = group_sum(ai[q], G, mask);
+      if (VAL) bm[q] = group_max(bm[q], G, mask);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        if (tb + q < t1) {
+          a.out[out_slot(a, tb + q)] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
+          if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+            flag_suspect(a.err);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Helmholtz S, compile-time order P.  h_n(kR) is built once per source by the
+// upward recurrence (_core.pyx:190-193) and shared by the targets; each target
+// carries c_n = (2n+1) j_n(k|t-c|) kappa_n from the prologue table.
+// ---------------------------------------------------------------------------
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
+  constexpr LegendreScale<P> L{};
+  const int G = a.G;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g = gt / G;
+  if (g >= a.n_ctr) return;
+  const int lane = (int)(threadIdx.x & (unsigned)(G - 1));
+  const unsigned mask = group_mask(G);
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int64_t b = a.nptr[g], e = a.nptr[g + 1];
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
+
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT], cf[NT][P + 1];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      const double ux = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      const double uy = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      const double uz = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(uz, uz, fma(uy, uy, ux * ux));
+      const double ir = r2[q] > 0.0 ? rsqrt(r2[q]) : 0.0;  // r = 0: cos g irrelevant
+      tx[q] = ux * ir;
+      ty[q] = uy * ir;
+      tz[q] = uz * ir;
+#pragma unroll
+      for (int n = 0; n <= P; ++n)
+        cf[q][n] = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    for (int64_t j = b + lane; j < e; j += G) {
+      const int s = __ldg(a.nidx + j);
+      const double4 q4 = ld256(a.sp + s);
+      const double wim = __ldg(a.swi + s);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt(R2);
+      const double x = k * (R2 * iR);
+      const double invx = iR * invk;
+      double hr[P + 1], hi[P + 1];
+      {
+        double h1r, h1i;
+        hankel01(k2 * R2, x, invx, hr[0], hi[0], h1r, h1i);
+        if constexpr (P >= 1) {
+          hr[1] = h1r;
+          hi[1] = h1i;
+        }
+      }
+#pragma unroll
+      for (int n = 1; n < P; ++n) {
+        const double f = (2.0 * n + 1.0) * invx;
+        hr[n + 1] = fma(f, hr[n], -hr[n - 1]);
+        hi[n + 1] = fma(f, hi[n], -hi[n - 1]);
+      }
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const double cg = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
+        double sr = cf[q][0] * hr[0], si = cf[q][0] * hi[0];
+        if constexpr (P >= 1) {
+          double pm = 1.0, pc = cg;
+          double c1 = cf[q][1] * pc;
+          sr = fma(c1, hr[1], sr);
+          si = fma(c1, hi[1], si);
+#pragma unroll
+          for (int n = 1; n < P; ++n) {
+            const double pn = fma(L.alpha[n] * cg, pc, -pm);
+            pm = pc;
+            pc = pn;
+            const double cn = cf[q][n + 1] * pc;
+            sr = fma(cn, hr[n + 1], sr);
+            si = fma(cn, hi[n + 1], si);
+          }
+        }
+        ar[q] = fma(q4.w, sr, fma(-wim, si, ar[q]));
+        ai[q] = fma(q4.w, si, fma(wim, sr, ai[q]));
+        if (VAL) bm[q] = fmax(bm[q], r2[q] * (iR * iR));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      ar[q] = group_sum(ar[q], G, mask);
+      ai[q] = group_sum(ai[q], G, mask);
+      if (VAL) bm[q] = group_max(bm[q], G, mask);
+    }
+    if (lane == 0) {
+      const double pk = k * kInvFourPi;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        if (tb + q < t1) {
+          a.out[out_slot(a, tb + q)] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) * acc
+          if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+            flag_suspect(a.err);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic kernel: runtime order, every variant, reference operation order
+// (_core.pyx:229-306 and :365-418).  One target per pass.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) generic_kernel(const EvalParams a, int equation) {
+  const int G = a.G;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g = gt / G;
+  if (g >= a.n_ctr) return;
+  const int lane = (int)(threadIdx.x & (unsigned)(G - 1));
+  const unsigned mask = group_mask(G);
+  const double c[3] = {a.ctr[3 * g], a.ctr[3 * g + 1], a.ctr[3 * g + 2]};
+  const int64_t b = a.nptr[g], e = a.nptr[g + 1];
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const int p = a.p, variant = a.variant;
+  const double k = a.k;
+
+  for (int64_t it = t0; it < t1; ++it) {
+    const double tc[3] = {a.tgt[3 * it] - c[0], a.tgt[3 * it + 1] - c[1],
+                          a.tgt[3 * it + 2] - c[2]};
+    const double r = sqrt(tc[0] * tc[0] + tc[1] * tc[1] + tc[2] * tc[2]);
+    double th[3] = {0.0, 0.0, 0.0};
+    if (r > 0.0) {
+      th[0] = tc[0] / r;
+      th[1] = tc[1] / r;
+      th[2] = tc[2] / r;
+    }
+    double nt[3] = {0.0, 0.0, 0.0};
+    if (a.tnrm) {
+      nt[0] = a.tnrm[3 * it];
+      nt[1] = a.tnrm[3 * it + 1];
+      nt[2] = a.tnrm[3 * it + 2];
+    }
+    const double* jt = equation ? a.ttab + it * a.ttab_stride : nullptr;
+    const double* jtp = equation ? jt + (p + 1) : nullptr;
+    double accr = 0.0, acci = 0.0, bmax = 0.0;
+    for (int64_t j = b + lane; j < e; j += G) {
+      const int s = a.nidx[j];
+      const double4 q4 = a.sp[s];
+      const double wim = a.swi[s];
+      const double sc[3] = {q4.x - c[0], q4.y - c[1], q4.z - c[2]};
+      const double R = sqrt(sc[0] * sc[0] + sc[1] * sc[1] + sc[2] * sc[2]);
+      const double sh[3] = {sc[0] / R, sc[1] / R, sc[2] / R};
+      double cg = 1.0;
+      if (r > 0.0) cg = fmin(1.0, fmax(-1.0, sh[0] * th[0] + sh[1] * th[1] + sh[2] * th[2]));
+      const double rho = r / R;
+      if (a.validate) bmax = fmax(bmax, rho * rho);
+      double ns[3] = {0.0, 0.0, 0.0};
+      if (variant == 2) {
+        const double4 n4 = a.snrm[s];
+        ns[0] = n4.x;
+        ns[1] = n4.y;
+        ns[2] = n4.z;
+      }
+      double sre = 0.0, sim = 0.0;
+      if (equation == 0) {
+        double sum = 0.0;
+        if (variant == 0) {
+          double rad = 1.0 / R, pm1 = 1.0, pc = cg;
+          sum = rad;
+          if (p >= 1) {
+            rad *= rho;
+            sum += rad * pc;
+          }
+          for (int n = 1; n < p; ++n) {
+            const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+            pm1 = pc;
+            pc = pn;
+            rad *= rho;
+            sum += rad * pc;
+          }
+        } else if (variant == 1) {
+          const double nt_sh = nt[0] * sh[0] + nt[1] * sh[1] + nt[2] * sh[2];
+          const double nt_th = r > 0.0 ? nt[0] * th[0] + nt[1] * th[1] + nt[2] * th[2] : nt_sh;
+          double rad = 1.0 / (R * R), pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
+          for (int n = 1; n <= p; ++n) {
+            sum += rad * (n * nt_th * pc + (nt_sh - nt_th * cg) * dc);
+            if (n < p) {
+              const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+              const double dn = dm1 + (2 * n + 1) * pc;
+              pm1 = pc;
+              pc = pn;
+              dm1 = dc;
+              dc = dn;
+              rad *= rho;
+            }
+          }
+        } else {
+          const double ns_sh = ns[0] * sh[0] + ns[1] * sh[1] + ns[2] * sh[2];
+          const double ns_th = r > 0.0 ? ns[0] * th[0] + ns[1] * th[1] + ns[2] * th[2] : ns_sh;
+          double rad = 1.0 / (R * R), pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
+          sum = rad * (-1.0 * ns_sh);
+          for (int n = 1; n <= p; ++n) {
+            rad *= rho;
+            sum += rad * (-(n + 1.0) * ns_sh * pc + (ns_th - ns_sh * cg) * dc);
+            if (n < p) {
+              const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+              const double dn = dm1 + (2 * n + 1) * pc;
+              pm1 = pc;
+              pc = pn;
+              dm1 = dc;
+              dc = dn;
+            }
+          }
+        }
+        sre = sum;
+      } else {
+        // h_0..h_{p+1}(kR) upward (_core.pyx:190-193), h'_n (:195-198)
+        double hr[TSQBX_MAX_ORDER + 2], hi[TSQBX_MAX_ORDER + 2];
+        const double x = k * R;
+        double sn, cs;
+        sincos(x, &sn, &cs);
+        hr[0] = sn / x;
+        hi[0] = -cs / x;
+        hr[1] = hr[0] / x + hi[0];   // h0 (1/x - i)
+        hi[1] = hi[0] / x - hr[0];
+        for (int n = 1; n <= p; ++n) {
+          const double f = (2.0 * n + 1.0) / x;
+          hr[n + 1] = f * hr[n] - hr[n - 1];
+          hi[n + 1] = f * hi[n] - hi[n - 1];
+        }
+        double pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
+        const double nt_sh = nt[0] * sh[0] + nt[1] * sh[1] + nt[2] * sh[2];
+        const double nt_th = nt[0] * th[0] + nt[1] * th[1] + nt[2] * th[2];
+        const double ns_sh = ns[0] * sh[0] + ns[1] * sh[1] + ns[2] * sh[2];
+        const double ns_th = r > 0.0 ? ns[0] * th[0] + ns[1] * th[1] + ns[2] * th[2] : ns_sh;
+        for (int n = 0; n <= p; ++n) {
+          const double pn = n == 0 ? 1.0 : pc;
+          const double dn = n == 0 ? 0.0 : dc;
+          if (n >= 1 && n < p) {
+            const double pnx = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+            const double dnx = dm1 + (2 * n + 1) * pc;
+            pm1 = pc;
+            pc = pnx;
+            dm1 = dc;
+            dc = dnx;
+          }
+          const double tw = 2.0 * n + 1.0;
+          if (variant == 0) {
+            const double f = tw * jt[n] * pn;
+            sre += f * hr[n];
+            sim += f * hi[n];
+          } else if (variant == 1) {
+            double f;
+            if (r > 0.0)
+              f = tw * (k * nt_th * jtp[n] * pn + (nt_sh - nt_th * cg) * jt[n] * dn / r);
+            else
+              f = tw * k * nt_sh * jtp[n] * pn;
+            sre += f * hr[n];
+            sim += f * hi[n];
+          } else {
+            double hpr, hpi;
+            if (n == 0) {
+              hpr = -hr[1];
+              hpi = -hi[1];
+            } else {
+              hpr = hr[n - 1] - (n + 1.0) / x * hr[n];
+              hpi = hi[n - 1] - (n + 1.0) / x * hi[n];
+            }
+            const double f1 = tw * jt[n] * k * ns_sh * pn;
+            const double f2 = tw * jt[n] * (ns_th - ns_sh * cg) * dn / R;
+            sre += f1 * hpr + f2 * hr[n];
+            sim += f1 * hpi + f2 * hi[n];
+          }
+        }
+      }
+      accr += q4.w * sre - wim * sim;
+      acci += q4.w * sim + wim * sre;
+    }
+    accr = group_sum(accr, G, mask);
+    acci = group_sum(acci, G, mask);
+    if (a.validate) bmax = group_max(bmax, G, mask);
+    if (lane == 0) {
+      double2 o;
+      if (equation == 0) {
+        o = make_double2(accr / kFourPi, acci / kFourPi);
+      } else {
+        const double pk = k / kFourPi;
+        o = make_double2(-acci * pk, accr * pk);
+      }
+      a.out[out_slot(a, it)] = o;
+      if (a.validate && (!isfinite(accr) || !isfinite(acci) || bmax > kSepScreen))
+        flag_suspect(a.err);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Helmholtz per-target prologue: one thread per center, loops over its targets.
+// mode 0 (fast S):   tab[n] = (2n+1) j_n(k r) kappa_n,        n <= p
+// mode 1 (generic):  tab[n] = j_n(k r), tab[p+1+n] = j'_n(k r)  (_core.pyx:354-359)
+// ---------------------------------------------------------------------------
+__global__ void helmholtz_target_table(const double* __restrict__ ctr, int64_t n_ctr,
+                                       const double* __restrict__ tgt,
+                                       const int64_t* __restrict__ tptr, int p, double k,
+                                       int mode, double* __restrict__ tab, int stride) {
+  const int64_t ic = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ic >= n_ctr) return;
+  double j[TSQBX_MAX_ORDER + 2];
+  for (int64_t it = tptr[ic]; it < tptr[ic + 1]; ++it) {
+    const double dx = tgt[3 * it] - ctr[3 * ic], dy = tgt[3 * it + 1] - ctr[3 * ic + 1],
+                 dz = tgt[3 * it + 2] - ctr[3 * ic + 2];
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    double* row = tab + it * stride;
+    if (r > 0.0) {
+      const double x = k * r;
+      miller_j(p + 2, x, j);
+      if (mode == 0) {
+        double km1 = 1.0, kc = 1.0;  // kappa_{n-1}, kappa_n
+        for (int n = 0; n <= p; ++n) {
+          const double kap = n == 0 ? 1.0 : kc;
+          row[n] = (2.0 * n + 1.0) * j[n] * kap;
+          if (n >= 1) {
+            const double kn = (double(n) / double(n + 1)) * km1;
+            km1 = kc;
+            kc = kn;
+          }
+        }
+      } else {
+        for (int n = 0; n <= p; ++n) row[n] = j[n];
+        row[p + 1] = -j[1];
+        for (int n = 1; n <= p; ++n) row[p + 1 + n] = j[n - 1] - (n + 1.0) / x * j[n];
+      }
+    } else {
+      for (int n = 0; n < stride; ++n) row[n] = 0.0;
+      row[0] = 1.0;
+      if (mode == 1 && p >= 1) row[p + 2] = 1.0 / 3.0;  // j'_1(0) = 1/3
+    }
+  }
+}
+
+__global__ void fp64_probe_kernel(double* out, int64_t iters) {
+  const double a = 1.0 + 1e-9 * threadIdx.x, b = -1e-12;
+  double x0 = 1.0, x1 = 2.0, x2 = 3.0, x3 = 4.0, x4 = 5.0, x5 = 6.0, x6 = 7.0, x7 = 8.0;
+  for (int64_t i = 0; i < iters; ++i) {
+    x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+    x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+  }
+  out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+__global__ void set_key(unsigned long long* key, unsigned long long v) { *key = v; }
+
+// ---------------------------------------------------------------------------
+// exact validation in the reference arithmetic (tsqbx.py:43-53): no FMA.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double norm_ref(double x, double y, double z) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+__global__ void validate_kernel(const double4* __restrict__ sp, const double* __restrict__ ctr,
+                                int64_t n_ctr, const int64_t* __restrict__ nptr,
+                                const int32_t* __restrict__ nidx,
+                                const double* __restrict__ tgt,
+                                const int64_t* __restrict__ tptr,
+                                unsigned long long* err) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= n_ctr) return;
+  const double cx = ctr[3 * g], cy = ctr[3 * g + 1], cz = ctr[3 * g + 2];
+  const int64_t b = nptr[g], e = nptr[g + 1];
+  for (int64_t it = tptr[g]; it < tptr[g + 1]; ++it) {
+    const double r = norm_ref(__dadd_rn(tgt[3 * it], -cx), __dadd_rn(tgt[3 * it + 1], -cy),
+                              __dadd_rn(tgt[3 * it + 2], -cz));
+    for (int64_t j = b + lane; j < e; j += 32) {
+      const double4 q = sp[nidx[j]];
+      const double R = norm_ref(__dadd_rn(q.x, -cx), __dadd_rn(q.y, -cy), __dadd_rn(q.z, -cz));
+      const unsigned long long pos = (unsigned long long)(j - b);
+      const unsigned long long base = (unsigned long long)it << 32;
+      if (R == 0.0) atomicMin(err, base | pos);
+      else if (__dmul_rn(R, 1.0 + 1e-12) < r) atomicMin(err, base | (1ull << 31) | pos);
+    }
+  }
+}
+
+__global__ void pack_kernel(int64_t n, const double* __restrict__ xyz,
+                            const double* __restrict__ w, const double* __restrict__ nrm,
+                            const int32_t* __restrict__ perm, double4* __restrict__ sp,
+                            double* __restrict__ swi, double4* __restrict__ snrm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = perm ? (int64_t)perm[i] : i;
+  sp[i] = make_double4(xyz[3 * s], xyz[3 * s + 1], xyz[3 * s + 2], w[2 * s]);
+  swi[i] = w[2 * s + 1];
+  if (nrm) snrm[i] = make_double4(nrm[3 * s], nrm[3 * s + 1], nrm[3 * s + 2], 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+constexpr int kMaxFastOrder = 16;
+
+template <int P, int NT, bool VAL>
+void launch_fast(int equation, const EvalParams& a, int blocks, cudaStream_t st) {
+  if (equation == TSQBX_EQ_LAPLACE)
+    laplace_s_kernel<P, NT, VAL><<<blocks, 256, 0, st>>>(a);
+  else
+    helmholtz_s_kernel<P, NT, VAL><<<blocks, 256, 0, st>>>(a);
+}
+
+template <int P>
+void launch_fast_p(int equation, int nt, bool val, const EvalParams& a, int blocks,
+                   cudaStream_t st) {
+  if (nt >= 2) {
+    if (val) launch_fast<P, 2, true>(equation, a, blocks, st);
+    else launch_fast<P, 2, false>(equation, a, blocks, st);
+  } else {
+    if (val) launch_fast<P, 1, true>(equation, a, blocks, st);
+    else launch_fast<P, 1, false>(equation, a, blocks, st);
+  }
+}
+
+template <int... Ps>
+struct FastTable {
+  static bool run(int p, int equation, int nt, bool val, const EvalParams& a, int blocks,
+                  cudaStream_t st) {
+    bool done = false;
+    ((p == Ps ? (launch_fast_p<Ps>(equation, nt, val, a, blocks, st), done = true) : false), ...);
+    return done;
+  }
+};
+using FastOrders = FastTable<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
+
+int64_t packed_doubles(int64_t n, int with_normals) {
+  const int64_t base = (5 * n + 3) / 4 * 4;  // keep the normals 32-byte aligned
+  return with_normals ? base + 4 * n : base;
+}
+
+}  // namespace tsqbx
+
+using namespace tsqbx;
+
+extern "C" {
+
+int tsqbx_abi_version(void) { return TSQBX_ABI_VERSION; }
+const char* tsqbx_last_error(void) { return g_err; }
+
+int tsqbx_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  int rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc) return rc;
+  if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return TSQBX_OK;
+}
+
+int64_t tsqbx_packed_doubles(int64_t n_src, int with_normals) {
+  return packed_doubles(n_src, with_normals);
+}
+
+int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const double* nrm,
+                       const int32_t* perm, double* packed, void* stream) {
+  if (n_src < 0 || (n_src > 0 && (!xyz || !w || !packed)))
+    return set_error(TSQBX_ERR_ARGUMENT, "pack_sources: bad arguments");
+  if (n_src == 0) return TSQBX_OK;
+  if (((uintptr_t)packed) & 31)
+    return set_error(TSQBX_ERR_ARGUMENT, "pack_sources: packed buffer must be 32-byte aligned");
+  const int64_t base = packed_doubles(n_src, 0);
+  double4* sp = reinterpret_cast<double4*>(packed);
+  double* swi = packed + 4 * n_src;
+  double4* sn = nrm ? reinterpret_cast<double4*>(packed + base) : nullptr;
+  const int blocks = (int)((n_src + 255) / 256);
+  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_src, xyz, w, nrm, perm, sp, swi, sn);
+  return check_cuda(cudaGetLastError(), "pack_kernel launch");
+}
+
+int64_t tsqbx_eval_workspace_bytes(int equation, int variant, int p, int64_t n_tgt) {
+  if (equation != TSQBX_EQ_HELMHOLTZ) return 0;
+  const int stride = (variant == 0 && p <= kMaxFastOrder) ? p + 1 : 2 * (p + 1);
+  return n_tgt * stride * (int64_t)sizeof(double) + 256;
+}
+
+int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* packed,
+                      int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
+                      const int64_t* near_ptr, const int32_t* near_idx, const double* tgt_xyz,
+                      const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
+                      const int64_t* tgt_out, int64_t out_offset, unsigned flags,
+                      int group_lanes, void* workspace, int64_t ws_bytes, double* out,
+                      int64_t* err_key, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (equation != TSQBX_EQ_LAPLACE && equation != TSQBX_EQ_HELMHOLTZ)
+    return set_error(TSQBX_ERR_ARGUMENT, "bad equation %d", equation);
+  if (variant < 0 || variant > 2) return set_error(TSQBX_ERR_ARGUMENT, "bad variant %d", variant);
+  if (p < 0 || p > TSQBX_MAX_ORDER)
+    return set_error(TSQBX_ERR_ARGUMENT, "order p=%d outside [0, %d]", p, TSQBX_MAX_ORDER);
+  if (equation == TSQBX_EQ_HELMHOLTZ && !(k > 0.0))
+    return set_error(TSQBX_ERR_ARGUMENT, "Helmholtz requires k > 0");
+  if (n_ctr < 0 || n_tgt < 0 || n_src < 0) return set_error(TSQBX_ERR_ARGUMENT, "negative size");
+  if (variant == 2 && !with_normals)
+    return set_error(TSQBX_ERR_ARGUMENT, "double-layer variant requires source normals");
+  if (variant == 1 && n_tgt > 0 && !tgt_nrm)
+    return set_error(TSQBX_ERR_ARGUMENT, "S' variant requires target normals");
+  const bool val = (flags & TSQBX_FLAG_VALIDATE) != 0;
+  if (val && !err_key) return set_error(TSQBX_ERR_ARGUMENT, "validation needs err_key");
+  if (n_src > INT32_MAX) return set_error(TSQBX_ERR_ARGUMENT, "n_src exceeds int32 indexing");
+  if (n_ctr > 0 && (!ctr_xyz || !near_ptr || !tgt_ptr || !out || (n_tgt > 0 && !tgt_xyz)))
+    return set_error(TSQBX_ERR_ARGUMENT, "null array");
+  int G = group_lanes <= 0 ? 8 : group_lanes;
+  if (G > 32 || (G & (G - 1))) return set_error(TSQBX_ERR_ARGUMENT, "group_lanes must be 1..32, pow2");
+  if (val) set_key<<<1, 1, 0, st>>>((unsigned long long*)err_key, (unsigned long long)TSQBX_ERR_KEY_NONE);
+  if (n_ctr == 0 || n_tgt == 0) return check_cuda(cudaGetLastError(), "eval");
+
+  const bool fast = variant == 0 && p <= kMaxFastOrder && !(flags & TSQBX_FLAG_GENERIC);
+  EvalParams a{};
+  a.sp = reinterpret_cast<const double4*>(packed);
+  a.swi = packed + 4 * n_src;
+  a.snrm = with_normals ? reinterpret_cast<const double4*>(packed + packed_doubles(n_src, 0))
+                        : nullptr;
+  a.ctr = ctr_xyz;
+  a.nptr = near_ptr;
+  a.nidx = near_idx;
+  a.tgt = tgt_xyz;
+  a.tnrm = tgt_nrm;
+  a.tptr = tgt_ptr;
+  a.tout = tgt_out;
+  a.out_offset = out_offset;
+  a.out = reinterpret_cast<double2*>(out);
+  a.err = (unsigned long long*)err_key;
+  a.n_ctr = n_ctr;
+  a.p = p;
+  a.variant = variant;
+  a.G = G;
+  a.validate = val ? 1 : 0;
+  a.k = k;
+  if (equation == TSQBX_EQ_HELMHOLTZ) {
+    a.ttab_stride = fast ? p + 1 : 2 * (p + 1);
+    const int64_t need = n_tgt * a.ttab_stride * (int64_t)sizeof(double);
+    if (!workspace || ws_bytes < need)
+      return set_error(TSQBX_ERR_ARGUMENT, "workspace too small: need %lld bytes", (long long)need);
+    a.ttab = static_cast<const double*>(workspace);
+    helmholtz_target_table<<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+        ctr_xyz, n_ctr, tgt_xyz, tgt_ptr, p, k, fast ? 0 : 1, static_cast<double*>(workspace),
+        a.ttab_stride);
+  }
+  if (fast) {
+    const int nt = n_tgt >= 2 * n_ctr ? 2 : 1;
+    const int blocks = (int)((n_ctr * G + 255) / 256);
+    FastOrders::run(p, equation, nt, val, a, blocks, st);
+  } else {
+    const int blocks = (int)((n_ctr * G + 127) / 128);
+    generic_kernel<<<blocks, 128, 0, st>>>(a, equation);
+  }
+  return check_cuda(cudaGetLastError(), "tsqbx eval launch");
+}
+
+int64_t tsqbx_user_workspace_bytes(int equation, int variant, int p, int64_t n_src,
+                                   int64_t n_tgt) {
+  const int64_t packed = packed_doubles(n_src, variant == 2) * (int64_t)sizeof(double);
+  return (packed + 255) / 256 * 256 + tsqbx_eval_workspace_bytes(equation, variant, p, n_tgt);
+}
+
+static int eval_user(int equation, int variant, double k, int p, const double* src_xyz,
+                     const double* src_w, const double* src_nrm, int64_t n_src,
+                     const double* ctr_xyz, int64_t n_ctr, const int64_t* near_ptr,
+                     const int32_t* near_idx, const double* tgt_xyz, const double* tgt_nrm,
+                     const int64_t* tgt_ptr, int64_t n_tgt, unsigned flags, void* workspace,
+                     int64_t ws_bytes, double* out, int64_t* err_key, void* stream) {
+  const int64_t need = tsqbx_user_workspace_bytes(equation, variant, p, n_src, n_tgt);
+  if (!workspace || ws_bytes < need)
+    return set_error(TSQBX_ERR_ARGUMENT, "workspace too small: need %lld bytes", (long long)need);
+  if (variant == 2 && !src_nrm)
+    return set_error(TSQBX_ERR_ARGUMENT, "double-layer variant requires source normals");
+  double* packed = static_cast<double*>(workspace);
+  const int64_t pbytes = (packed_doubles(n_src, variant == 2) * (int64_t)sizeof(double) + 255) /
+                         256 * 256;
+  int rc = tsqbx_pack_sources(n_src, src_xyz, src_w, variant == 2 ? src_nrm : nullptr, nullptr,
+                              packed, stream);
+  if (rc) return rc;
+  return tsqbx_eval_packed(equation, variant, k, p, packed, n_src, variant == 2, ctr_xyz, n_ctr,
+                           near_ptr, near_idx, tgt_xyz, tgt_nrm, tgt_ptr, n_tgt, nullptr, 0,
+                           flags, 0, static_cast<char*>(workspace) + pbytes, ws_bytes - pbytes,
+                           out, err_key, stream);
+}
+
+int tsqbx_eval_laplace(int variant, int p, const double* src_xyz, const double* src_w,
+                       const double* src_nrm, int64_t n_src, const double* ctr_xyz,
+                       int64_t n_ctr, const int64_t* near_ptr, const int32_t* near_idx,
+                       const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
+                       int64_t n_tgt, unsigned flags, void* workspace, int64_t ws_bytes,
+                       double* out, int64_t* err_key, void* stream) {
+  return eval_user(TSQBX_EQ_LAPLACE, variant, 0.0, p, src_xyz, src_w, src_nrm, n_src, ctr_xyz,
+                   n_ctr, near_ptr, near_idx, tgt_xyz, tgt_nrm, tgt_ptr, n_tgt, flags, workspace,
+                   ws_bytes, out, err_key, stream);
+}
+
+int tsqbx_eval_helmholtz(int variant, double k, int p, const double* src_xyz,
+                         const double* src_w, const double* src_nrm, int64_t n_src,
+                         const double* ctr_xyz, int64_t n_ctr, const int64_t* near_ptr,
+                         const int32_t* near_idx, const double* tgt_xyz, const double* tgt_nrm,
+                         const int64_t* tgt_ptr, int64_t n_tgt, unsigned flags, void* workspace,
+                         int64_t ws_bytes, double* out, int64_t* err_key, void* stream) {
+  return eval_user(TSQBX_EQ_HELMHOLTZ, variant, k, p, src_xyz, src_w, src_nrm, n_src, ctr_xyz,
+                   n_ctr, near_ptr, near_idx, tgt_xyz, tgt_nrm, tgt_ptr, n_tgt, flags, workspace,
+                   ws_bytes, out, err_key, stream);
+}
+
+int tsqbx_fp64_probe(double* out, int64_t iters, int blocks, int threads, void* stream) {
+  if (!out || iters <= 0 || blocks <= 0 || threads <= 0 || threads > 1024)
+    return set_error(TSQBX_ERR_ARGUMENT, "fp64_probe: bad arguments");
+  fp64_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(out, iters);
+  return check_cuda(cudaGetLastError(), "fp64_probe launch");
+}
+
+int tsqbx_validate(const double* packed, int64_t n_src, const double* ctr_xyz, int64_t n_ctr,
+                   const int64_t* near_ptr, const int32_t* near_idx,
+                   const double* tgt_xyz, const int64_t* tgt_ptr, int64_t n_tgt,
+                   int64_t* err_key, void* stream) {
+  (void)n_src;
+  (void)n_tgt;
+  if (!err_key) return set_error(TSQBX_ERR_ARGUMENT, "validate: err_key is null");
+  cudaStream_t st = (cudaStream_t)stream;
+  set_key<<<1, 1, 0, st>>>((unsigned long long*)err_key, (unsigned long long)TSQBX_ERR_KEY_NONE);
+  if (n_ctr > 0) {
+    const int blocks = (int)((n_ctr * 32 + 255) / 256);
+    validate_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const double4*>(packed), ctr_xyz,
+                                            n_ctr, near_ptr, near_idx, tgt_xyz,
+                                            tgt_ptr, (unsigned long long*)err_key);
+  }
+  return check_cuda(cudaGetLastError(), "validate launch");
+}
+
+}  // extern "C"

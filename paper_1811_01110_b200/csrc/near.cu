@@ -1,0 +1,497 @@
+// near.cu -- device radius-ball near-list (CSR) builder for sm_100a.
+//
+// BASELINE.json defines a center's near list as every source within a radius
+// of it (self included); the reference has no such builder (its driver uses
+// tree lists, driver.py:197-228 / ilists.py:93-218; the closest analogue is
+// cKDTree.query_ball_point, costmodel.py:361-365).
+//
+// Pipeline (all stream-ordered, no host sync until the caller reads n_pairs):
+//   1. bounding box + max radius           (warp-reduced ordered-int atomics)
+//   2. fine Morton keys of sources/centers  (21 bits/axis; coarse cell = fine >> 3)
+//   3. CUB radix sort of both               -> src_perm, ctr_order ("tree leaf" order)
+//   4. open-addressed hash: coarse cell -> [start, end) in the sorted sources
+//   5. count: one warp per center; lanes look up the 27 neighbour cells, a
+//      warp bitonic sort puts them in Morton order, lanes sweep each cell,
+//      ballot + popc count members
+//   6. CUB exclusive scan -> near_ptr, n_pairs
+//   7. fill: same sweep, ballot-ranked stores -> rows ascending in sorted order
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace tsqbx {
+namespace {
+
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr int kFineBits = 21;
+constexpr int kSubBits = 3;  // coarse cell = 8 fine cells per axis
+
+struct NearLayout {
+  size_t off_mm, off_prm, off_skey_in, off_skey, off_sval_in, off_ckey_in, off_ckey, off_cval_in,
+      off_sxyz, off_hkey, off_hst, off_hen, off_cnt, off_tmp, total;
+  int64_t cap;
+  size_t tmp_bytes;
+};
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+NearLayout near_layout(int64_t n_ctr, int64_t n_src) {
+  NearLayout L{};
+  int64_t cap = 1024;
+  while (cap < 2 * n_src) cap <<= 1;
+  L.cap = cap;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  L.off_mm = take(8 * sizeof(long long));
+  L.off_prm = take(8 * sizeof(double));
+  L.off_skey_in = take(n_src * sizeof(unsigned long long));
+  L.off_skey = take(n_src * sizeof(unsigned long long));
+  L.off_sval_in = take(n_src * sizeof(int32_t));
+  L.off_ckey_in = take(n_ctr * sizeof(unsigned long long));
+  L.off_ckey = take(n_ctr * sizeof(unsigned long long));
+  L.off_cval_in = take(n_ctr * sizeof(int32_t));
+  L.off_sxyz = take(n_src * sizeof(double4));
+  L.off_hkey = take(cap * sizeof(unsigned long long));
+  L.off_hst = take(cap * sizeof(int32_t));
+  L.off_hen = take(cap * sizeof(int32_t));
+  L.off_cnt = take((n_ctr + 1) * sizeof(int64_t));
+  size_t t1 = 0, t2 = 0, t3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)n_src, 0, 3 * kFineBits);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)n_ctr, 0, 3 * kFineBits);
+  cub::DeviceScan::ExclusiveSum(nullptr, t3, (int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)(n_ctr + 1));
+  L.tmp_bytes = std::max(t1, std::max(t2, t3)) + 256;
+  L.off_tmp = take(L.tmp_bytes);
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ long long ord_of(double d) {
+  const long long b = __double_as_longlong(d);
+  return b >= 0 ? b : b ^ 0x7fffffffffffffffLL;
+}
+__device__ __forceinline__ double of_ord(long long b) {
+  return __longlong_as_double(b >= 0 ? b : b ^ 0x7fffffffffffffffLL);
+}
+
+__device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ unsigned long long morton3(unsigned long long x, unsigned long long y,
+                                                      unsigned long long z) {
+  return spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
+}
+__device__ __forceinline__ unsigned long long hash64(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+__global__ void init_bounds(long long* mm) {
+  const int i = threadIdx.x;
+  if (i < 3) mm[i] = LLONG_MAX;                 // min x, y, z
+  else if (i < 6) mm[i] = LLONG_MIN;            // max x, y, z
+  else if (i == 6) mm[i] = LLONG_MIN;           // max radius
+}
+
+__global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
+                              const double* __restrict__ ctr, const double* __restrict__ rad,
+                              int64_t n_ctr, long long* mm) {
+  long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+  long long hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  long long rm = LLONG_MIN;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_src + n_ctr;
+       i += stride) {
+    const double* p = i < n_src ? src + 3 * i : ctr + 3 * (i - n_src);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const long long o = ord_of(p[d]);
+      lo[d] = min(lo[d], o);
+      hi[d] = max(hi[d], o);
+    }
+    if (i >= n_src) rm = max(rm, ord_of(rad[i - n_src]));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = min(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], off));
+      hi[d] = max(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], off));
+    }
+    rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      atomicMin(&mm[d], lo[d]);
+      atomicMax(&mm[3 + d], hi[d]);
+    }
+    atomicMax(&mm[6], rm);
+  }
+}
+
+// prm = {lo_x, lo_y, lo_z, fine cell}
+__global__ void grid_params(const long long* mm, double* prm) {
+  double lo[3], ext = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = of_ord(mm[d]);
+    ext = fmax(ext, of_ord(mm[3 + d]) - lo[d]);
+  }
+  const double rmax = mm[6] == LLONG_MIN ? 0.0 : of_ord(mm[6]);
+  // coarse cell >= rmax (with slack for rounding of the cell index) so the
+  // 27 neighbours of a center's cell cover its ball; 2^21 fine cells per axis max
+  double fine = fmax(rmax * (1.0 + 1e-9) / (1 << kSubBits),
+                     ext / (double)((1 << kFineBits) - 32));
+  if (!(fine > 0.0)) fine = 1.0;
+  prm[0] = lo[0];
+  prm[1] = lo[1];
+  prm[2] = lo[2];
+  prm[3] = fine;
+}
+
+__device__ __forceinline__ void fine_coords(const double* p, const double* prm,
+                                            unsigned long long* f) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double q = floor((p[d] - prm[d]) / prm[3]);
+    q = fmin(fmax(q, 0.0), (double)((1 << kFineBits) - 32));
+    f[d] = (unsigned long long)q + (1ull << kSubBits);  // coarse coordinate >= 1
+  }
+}
+
+__global__ void key_kernel(const double* __restrict__ pts, int64_t n, const double* prm,
+                           unsigned long long* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long f[3];
+  fine_coords(pts + 3 * i, prm, f);
+  key[i] = morton3(f[0], f[1], f[2]);
+  val[i] = (int32_t)i;
+}
+
+__global__ void gather_sorted(const double* __restrict__ src, const int32_t* __restrict__ perm,
+                              int64_t n, double4* __restrict__ sxyz) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = perm[i];
+  sxyz[i] = make_double4(src[3 * s], src[3 * s + 1], src[3 * s + 2], 0.0);
+}
+
+__global__ void hash_clear(unsigned long long* hkey, int64_t cap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cap) hkey[i] = kEmpty;
+}
+
+__device__ __forceinline__ int64_t hash_slot(unsigned long long* hkey, int64_t cap,
+                                             unsigned long long ck) {
+  int64_t h = (int64_t)(hash64(ck) & (unsigned long long)(cap - 1));
+  while (true) {
+    const unsigned long long prev = atomicCAS(&hkey[h], kEmpty, ck);
+    if (prev == kEmpty || prev == ck) return h;
+    h = (h + 1) & (cap - 1);
+  }
+}
+
+__global__ void hash_insert(const unsigned long long* __restrict__ skey, int64_t n,
+                            unsigned long long* hkey, int32_t* hst, int32_t* hen, int64_t cap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long ck = skey[i] >> (3 * kSubBits);
+  const bool head = i == 0 || (skey[i - 1] >> (3 * kSubBits)) != ck;
+  const bool tail = i == n - 1 || (skey[i + 1] >> (3 * kSubBits)) != ck;
+  if (!head && !tail) return;
+  const int64_t h = hash_slot(hkey, cap, ck);
+  if (head) hst[h] = (int32_t)i;
+  if (tail) hen[h] = (int32_t)(i + 1);
+}
+
+__device__ __forceinline__ bool hash_find(const unsigned long long* __restrict__ hkey,
+                                          const int32_t* __restrict__ hst,
+                                          const int32_t* __restrict__ hen, int64_t cap,
+                                          unsigned long long ck, int& st, int& en) {
+  int64_t h = (int64_t)(hash64(ck) & (unsigned long long)(cap - 1));
+  while (true) {
+    const unsigned long long k = hkey[h];
+    if (k == ck) {
+      st = hst[h];
+      en = hen[h];
+      return true;
+    }
+    if (k == kEmpty) return false;
+    h = (h + 1) & (cap - 1);
+  }
+}
+
+__device__ __forceinline__ bool member(const double4 s, double cx, double cy, double cz,
+                                       double rad2) {
+  const double dx = __dadd_rn(s.x, -cx), dy = __dadd_rn(s.y, -cy), dz = __dadd_rn(s.z, -cz);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return d2 <= rad2;
+}
+
+// one warp per center (processing order); FILL = false counts, true writes
+template <bool FILL>
+__global__ void __launch_bounds__(256) sweep_kernel(
+    const double* __restrict__ ctr, const double* __restrict__ rad, int64_t n_ctr,
+    const int32_t* __restrict__ order, const double* __restrict__ prm,
+    const double4* __restrict__ sxyz, const unsigned long long* __restrict__ hkey,
+    const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
+    int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= n_ctr) return;
+  const int64_t ic = order[g];
+  const double cx = ctr[3 * ic], cy = ctr[3 * ic + 1], cz = ctr[3 * ic + 2];
+  const double r = rad[ic];
+  const double rad2 = __dmul_rn(r, r);
+  double pl[3] = {cx, cy, cz};
+  double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
+  unsigned long long f[3];
+  fine_coords(pl, prm_l, f);
+  const unsigned long long ccx = f[0] >> kSubBits, ccy = f[1] >> kSubBits, ccz = f[2] >> kSubBits;
+
+  unsigned long long key = kEmpty;
+  int st = 0, en = 0;
+  if (lane < 27) {
+    const unsigned long long nk =
+        morton3(ccx + (lane / 9) - 1, ccy + ((lane / 3) % 3) - 1, ccz + (lane % 3) - 1);
+    if (hash_find(hkey, hst, hen, cap, nk, st, en)) key = nk;
+  }
+  // warp bitonic sort of the neighbour cells by Morton key (ascending)
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, stride);
+      const int os = __shfl_xor_sync(0xffffffffu, st, stride);
+      const int oe = __shfl_xor_sync(0xffffffffu, en, stride);
+      const bool up = (lane & size) == 0 || size == 32;
+      const bool lower = (lane & stride) == 0;
+      const bool take = (lower == up) ? (ok < key) : (ok > key);
+      if (take) {
+        key = ok;
+        st = os;
+        en = oe;
+      }
+    }
+  }
+  int64_t count = 0;
+  int64_t out = FILL ? nptr[g] : 0;
+  for (int L = 0; L < 27; ++L) {
+    const unsigned long long k = __shfl_sync(0xffffffffu, key, L);
+    if (k == kEmpty) break;
+    const int cs = __shfl_sync(0xffffffffu, st, L);
+    const int ce = __shfl_sync(0xffffffffu, en, L);
+    for (int base = cs; base < ce; base += 32) {
+      const int j = base + lane;
+      const bool m = j < ce && member(sxyz[j], cx, cy, cz, rad2);
+      const unsigned bal = __ballot_sync(0xffffffffu, m);
+      if (FILL && m) nidx[out + __popc(bal & ((1u << lane) - 1u))] = j;
+      out += __popc(bal);
+      count += __popc(bal);
+    }
+  }
+  if (!FILL && lane == 0) cnt[g] = count;
+}
+
+__global__ void set_tail(int64_t* cnt, int64_t n) { cnt[n] = 0; }
+
+// --- targets into processing order -------------------------------------------
+__global__ void order_count(const int32_t* __restrict__ order, const int64_t* __restrict__ tptr,
+                            int64_t n, int64_t* __restrict__ cnt) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > n) return;
+  if (g == n) {
+    cnt[n] = 0;
+    return;
+  }
+  const int64_t ic = order[g];
+  cnt[g] = tptr[ic + 1] - tptr[ic];
+}
+
+__global__ void order_copy(const int32_t* __restrict__ order, const double* __restrict__ ctr,
+                           const int64_t* __restrict__ tptr, const double* __restrict__ tgt,
+                           const double* __restrict__ tnrm, int64_t n,
+                           const int64_t* __restrict__ tptr_out, double* __restrict__ ctr_out,
+                           double* __restrict__ tgt_out, double* __restrict__ tnrm_out,
+                           int64_t* __restrict__ tidx) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const int64_t ic = order[g];
+  ctr_out[3 * g] = ctr[3 * ic];
+  ctr_out[3 * g + 1] = ctr[3 * ic + 1];
+  ctr_out[3 * g + 2] = ctr[3 * ic + 2];
+  const int64_t src0 = tptr[ic], cnt = tptr[ic + 1] - src0, dst0 = tptr_out[g];
+  for (int64_t j = 0; j < cnt; ++j) {
+    for (int d = 0; d < 3; ++d) {
+      tgt_out[3 * (dst0 + j) + d] = tgt[3 * (src0 + j) + d];
+      if (tnrm) tnrm_out[3 * (dst0 + j) + d] = tnrm[3 * (src0 + j) + d];
+    }
+    tidx[dst0 + j] = src0 + j;
+  }
+}
+
+__global__ void scatter_c128(int64_t n, const int64_t* __restrict__ dest,
+                             const double2* __restrict__ src, double2* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[dest ? dest[i] : i] = src[i];
+}
+
+}  // namespace
+}  // namespace tsqbx
+
+using namespace tsqbx;
+
+extern "C" {
+
+int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src) {
+  if (n_ctr < 0 || n_src < 0) return -1;
+  return (int64_t)near_layout(n_ctr, n_src).total;
+}
+
+int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                     const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
+                     int32_t* src_perm, int32_t* ctr_order, int64_t* near_ptr, int64_t* n_pairs,
+                     void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_ctr < 0 || n_src < 0 || n_src > INT32_MAX - 64 || n_ctr > INT32_MAX - 64)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_count: bad sizes");
+  const NearLayout L = near_layout(n_ctr, n_src);
+  if (!workspace || ws_bytes < (int64_t)L.total)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_count: workspace too small (need %lld)",
+                     (long long)L.total);
+  if (!near_ptr || !n_pairs || (n_ctr > 0 && (!ctr_xyz || !radius || !ctr_order)) ||
+      (n_src > 0 && (!src_xyz || !src_perm)))
+    return set_error(TSQBX_ERR_ARGUMENT, "near_count: null array");
+  char* ws = static_cast<char*>(workspace);
+  long long* mm = reinterpret_cast<long long*>(ws + L.off_mm);
+  double* prm = reinterpret_cast<double*>(ws + L.off_prm);
+  auto* skey_in = reinterpret_cast<unsigned long long*>(ws + L.off_skey_in);
+  auto* skey = reinterpret_cast<unsigned long long*>(ws + L.off_skey);
+  auto* sval_in = reinterpret_cast<int32_t*>(ws + L.off_sval_in);
+  auto* ckey_in = reinterpret_cast<unsigned long long*>(ws + L.off_ckey_in);
+  auto* ckey = reinterpret_cast<unsigned long long*>(ws + L.off_ckey);
+  auto* cval_in = reinterpret_cast<int32_t*>(ws + L.off_cval_in);
+  auto* sxyz = reinterpret_cast<double4*>(ws + L.off_sxyz);
+  auto* hkey = reinterpret_cast<unsigned long long*>(ws + L.off_hkey);
+  auto* hst = reinterpret_cast<int32_t*>(ws + L.off_hst);
+  auto* hen = reinterpret_cast<int32_t*>(ws + L.off_hen);
+  auto* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
+  void* tmp = ws + L.off_tmp;
+
+  init_bounds<<<1, 32, 0, st>>>(mm);
+  if (n_src + n_ctr > 0) {
+    int nb = (int)std::min<int64_t>((n_src + n_ctr + 255) / 256, 148 * 8);
+    bounds_kernel<<<nb, 256, 0, st>>>(src_xyz, n_src, ctr_xyz, radius, n_ctr, mm);
+  }
+  grid_params<<<1, 1, 0, st>>>(mm, prm);
+  size_t tb = L.tmp_bytes;
+  if (n_src > 0) {
+    key_kernel<<<(int)((n_src + 255) / 256), 256, 0, st>>>(src_xyz, n_src, prm, skey_in, sval_in);
+    cub::DeviceRadixSort::SortPairs(tmp, tb, skey_in, skey, sval_in, src_perm, (int)n_src, 0,
+                                    3 * kFineBits, st);
+    gather_sorted<<<(int)((n_src + 255) / 256), 256, 0, st>>>(src_xyz, src_perm, n_src, sxyz);
+  }
+  hash_clear<<<(int)((L.cap + 255) / 256), 256, 0, st>>>(hkey, L.cap);
+  if (n_src > 0)
+    hash_insert<<<(int)((n_src + 255) / 256), 256, 0, st>>>(skey, n_src, hkey, hst, hen, L.cap);
+  if (n_ctr > 0) {
+    key_kernel<<<(int)((n_ctr + 255) / 256), 256, 0, st>>>(ctr_xyz, n_ctr, prm, ckey_in, cval_in);
+    tb = L.tmp_bytes;
+    cub::DeviceRadixSort::SortPairs(tmp, tb, ckey_in, ckey, cval_in, ctr_order, (int)n_ctr, 0,
+                                    3 * kFineBits, st);
+    sweep_kernel<false><<<(int)((n_ctr * 32 + 255) / 256), 256, 0, st>>>(
+        ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, cnt, nullptr,
+        nullptr);
+  }
+  set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
+  tb = L.tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
+  cudaError_t e = cudaMemcpyAsync(n_pairs, near_ptr + n_ctr, sizeof(int64_t),
+                                  cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "near_count copy");
+  return check_cuda(cudaGetLastError(), "near_count launch");
+}
+
+int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                    const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
+                    const int32_t* ctr_order, const int64_t* near_ptr, int32_t* near_idx,
+                    void* stream) {
+  (void)src_xyz;
+  cudaStream_t st = (cudaStream_t)stream;
+  const NearLayout L = near_layout(n_ctr, n_src);
+  if (!workspace || ws_bytes < (int64_t)L.total)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_fill: workspace too small");
+  if (n_ctr == 0) return TSQBX_OK;
+  char* ws = static_cast<char*>(workspace);
+  sweep_kernel<true><<<(int)((n_ctr * 32 + 255) / 256), 256, 0, st>>>(
+      ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
+      reinterpret_cast<const double4*>(ws + L.off_sxyz),
+      reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
+      reinterpret_cast<const int32_t*>(ws + L.off_hst),
+      reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, nullptr, near_ptr, near_idx);
+  return check_cuda(cudaGetLastError(), "near_fill launch");
+}
+
+int64_t tsqbx_order_workspace_bytes(int64_t n_ctr) {
+  if (n_ctr < 0) return -1;
+  size_t t = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)(n_ctr + 1));
+  return (int64_t)(align256((n_ctr + 1) * sizeof(int64_t)) + align256(t));
+}
+
+int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* ctr_xyz,
+                        const int64_t* tgt_ptr, const double* tgt_xyz, const double* tgt_nrm,
+                        int64_t n_tgt, void* workspace, int64_t ws_bytes, double* ctr_out,
+                        int64_t* tptr_out, double* tgt_out, double* tnrm_out, int64_t* tgt_index,
+                        void* stream) {
+  (void)n_tgt;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_ctr < 0 || ws_bytes < tsqbx_order_workspace_bytes(n_ctr) || !workspace)
+    return set_error(TSQBX_ERR_ARGUMENT, "order_targets: bad sizes or workspace");
+  if (n_ctr > 0 && (!ctr_order || !ctr_xyz || !tgt_ptr || !ctr_out || !tptr_out || !tgt_index ||
+                    (tgt_nrm && !tnrm_out)))
+    return set_error(TSQBX_ERR_ARGUMENT, "order_targets: null array");
+  char* ws = static_cast<char*>(workspace);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws);
+  void* tmp = ws + align256((n_ctr + 1) * sizeof(int64_t));
+  size_t tb = (size_t)ws_bytes - align256((n_ctr + 1) * sizeof(int64_t));
+  order_count<<<(int)((n_ctr + 256) / 256), 256, 0, st>>>(ctr_order, tgt_ptr, n_ctr, cnt);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, tptr_out, (int)(n_ctr + 1), st);
+  if (n_ctr > 0)
+    order_copy<<<(int)((n_ctr + 255) / 256), 256, 0, st>>>(ctr_order, ctr_xyz, tgt_ptr, tgt_xyz,
+                                                            tgt_nrm, n_ctr, tptr_out, ctr_out,
+                                                            tgt_out, tnrm_out, tgt_index);
+  return check_cuda(cudaGetLastError(), "order_targets launch");
+}
+
+int tsqbx_scatter_c128(int64_t n, const int64_t* dest, const double* src, double* out,
+                       void* stream) {
+  if (n < 0 || (n > 0 && (!src || !out)))
+    return set_error(TSQBX_ERR_ARGUMENT, "scatter_c128: bad arguments");
+  if (n == 0) return TSQBX_OK;
+  scatter_c128<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      n, dest, reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(out));
+  return check_cuda(cudaGetLastError(), "scatter_c128 launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+"""Near-list construction on the device.
+
+BASELINE.json defines a QBX center's near field as every source within a
+radius of it (self included).  The reference has no such builder -- its driver
+gathers tree lists per target box (driver.py:197-228, ilists.py:93-218) and
+uses ``cKDTree.query_ball_point`` elsewhere (costmodel.py:361-365) -- so
+``build_near_lists`` is the device replacement for that step:
+
+* sources and centers are Morton-sorted ("tree leaf" order) so that the
+  centers one CTA evaluates share a source neighbourhood,
+* the CSR rows are stored in that processing order and index the sorted
+  sources, ascending within a row,
+* membership is ``((dx*dx + dy*dy) + dz*dz) <= rad*rad`` without FMA
+  contraction, bit-identical to the oracle (``oracle.near_csr``).
+
+A user-supplied CSR (user center rows, user source indices) is accepted too
+(``NearLists.from_user_csr``); it is evaluated in place without reordering.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+
+
+@dataclass
+class NearLists:
+    """Device CSR from centers to near sources.
+
+    ptr[g]..ptr[g+1] is the row of center ``ctr_order[g]`` (identity when
+    ``ctr_order`` is None); idx entries index the sources in *packed* order,
+    i.e. user source ``src_perm[idx]`` (identity when ``src_perm`` is None).
+    """
+
+    n_ctr: int
+    n_src: int
+    n_pairs: int
+    ptr: torch.Tensor
+    idx: torch.Tensor
+    src_perm: torch.Tensor | None = None
+    ctr_order: torch.Tensor | None = None
+
+    @property
+    def mean_len(self) -> float:
+        return self.n_pairs / max(1, self.n_ctr)
+
+    @classmethod
+    def from_user_csr(cls, ptr, idx, n_src: int, device=None) -> "NearLists":
+        dev = dv.require_cuda(device)
+        p = dv.to_device(ptr, torch.int64, dev)
+        i = dv.to_device(idx, torch.int32, dev)
+        n_ctr = int(p.shape[0]) - 1
+        n_pairs = int(i.shape[0])
+        return cls(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=p, idx=i)
+
+    def to_user_csr(self) -> tuple[np.ndarray, np.ndarray]:
+        """(ptr, idx) on the host with rows by user center and user source indices."""
+        ptr = self.ptr.cpu().numpy()
+        idx = self.idx.cpu().numpy()
+        if self.src_perm is not None:
+            idx = self.src_perm.cpu().numpy()[idx]
+        if self.ctr_order is None:
+            return ptr, idx.astype(np.int32)
+        order = self.ctr_order.cpu().numpy()
+        lens = np.diff(ptr)
+        user_lens = np.empty_like(lens)
+        user_lens[order] = lens
+        uptr = np.zeros(self.n_ctr + 1, dtype=np.int64)
+        np.cumsum(user_lens, out=uptr[1:])
+        uidx = np.empty_like(idx)
+        dest = np.repeat(uptr[order] - ptr[:-1], lens) + np.arange(idx.shape[0])
+        uidx[dest] = idx
+        return uptr, uidx.astype(np.int32)
+
+
+def build_near_lists(centers, sources, radii, device=None) -> NearLists:
+    """Radius-ball near lists {s : |s - c|^2 <= rad_c^2} on the device.
+
+    centers (n_ctr, 3), sources (n_src, 3), radii scalar or (n_ctr,) -- numpy
+    arrays or torch tensors.  Returns a device :class:`NearLists` in Morton
+    processing order.
+    """
+    dev = dv.require_cuda(device)
+    L = _lib.load()
+    ctr = dv.to_device(centers, torch.float64, dev, (-1, 3))
+    src = dv.to_device(sources, torch.float64, dev, (-1, 3))
+    n_ctr, n_src = int(ctr.shape[0]), int(src.shape[0])
+    if isinstance(radii, torch.Tensor):
+        rad = radii.to(device=dev, dtype=torch.float64).reshape(-1).contiguous()
+        if rad.numel() == 1:
+            rad = rad.expand(n_ctr).contiguous()
+    else:
+        rad = dv.to_device(np.broadcast_to(np.asarray(radii, dtype=np.float64), (n_ctr,)),
+                           torch.float64, dev)
+    st = dv.stream_handle(dev)
+    ws_bytes = int(L.tsqbx_near_workspace_bytes(n_ctr, n_src))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    src_perm = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
+    ctr_order = torch.empty(max(n_ctr, 1), dtype=torch.int32, device=dev)
+    nptr = torch.empty(n_ctr + 1, dtype=torch.int64, device=dev)
+    npairs = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.check(L.tsqbx_near_count(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
+                                  ws.data_ptr(), ws_bytes, src_perm.data_ptr(),
+                                  ctr_order.data_ptr(), nptr.data_ptr(), npairs.data_ptr(), st),
+               "tsqbx_near_count")
+    n_pairs = int(npairs.item())
+    idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
+    _lib.check(L.tsqbx_near_fill(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
+                                 ws.data_ptr(), ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
+                                 idx.data_ptr(), st),
+               "tsqbx_near_fill")
+    return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr, idx=idx[:n_pairs],
+                     src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr])

@@ -1,0 +1,337 @@
+"""Target-specific QBX (TSQBX) evaluation on B200.
+
+Drop-in for the reference's public TSQBX API
+(/root/reference/pkg/src/gigaqbx/tsqbx.py:28-92):
+
+* ``TsConfig``, ``ts_accumulate`` and ``ts_eval`` keep the reference's names,
+  argument meaning, return type and error behaviour (``ValueError`` texts of
+  ``_prep``, tsqbx.py:38-65), but evaluate on the GPU through the C ABI.
+* ``ts_accumulate_batch`` is the batched form the hardware needs: every center
+  with its CSR row of near sources and its run of targets in ONE launch,
+  returning per-target potentials.
+* ``TsqbxProblem`` keeps a whole problem resident in HBM for repeated
+  evaluation (the bench's device-resident measurement).
+
+Validation (``validate=True``) runs on the device: the kernel screens every
+pair (``rho^2 > (1+1e-12)^2`` or a non-finite result), and only a flagged
+launch runs the exact reference predicate (``tsqbx_validate``) to name the
+offending source.  The driver-style path (``driver._ts_accum``,
+driver.py:383-389) does no validation; ``validate=False`` matches it.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+from .kernels import Equation, KernelSpec
+from .nearlist import NearLists
+
+_SEP_SLACK = 1e-12
+
+
+@dataclass(frozen=True)
+class TsConfig:
+    """Same as tsqbx.py:28-35."""
+
+    spec: KernelSpec
+    p_qbx: int
+
+    def __post_init__(self):
+        if self.p_qbx < 0:
+            raise ValueError("p_qbx must be nonnegative")
+
+
+def pick_group_lanes(mean_len: float) -> int:
+    """Lanes that share one center: ~4 list entries per lane, power of two in [1, 32]."""
+    env = os.environ.get("GIGAQBX_GROUP_LANES")
+    if env:
+        return int(env)
+    g = 1 << max(0, int(round(math.log2(max(1.0, mean_len / 4.0)))))
+    return max(1, min(32, g))
+
+
+def _equation_code(spec: KernelSpec) -> int:
+    return _lib.EQ_LAPLACE if spec.equation is Equation.LAPLACE else _lib.EQ_HELMHOLTZ
+
+
+class _Prepared:
+    """Device-side inputs of one evaluation, in processing order.
+
+    Sources are packed (and Morton-permuted when the near lists come from
+    ``build_near_lists``); centers, target runs and targets are reordered to
+    the CSR's row order so that row g, its targets and its near sources are
+    all addressed by g (what lets a rank evaluate a contiguous row range).
+    """
+
+    def __init__(self, cfg: TsConfig, dev, src, w, sn, ctr, near: NearLists, tgt, tn, tptr,
+                 group_lanes=None):
+        L = _lib.load()
+        self.cfg, self.dev, self.near = cfg, dev, near
+        self.src, self.w, self.sn = src, w, sn
+        self.user_ctr, self.user_tgt = ctr, tgt
+        self.n_src = int(src.shape[0])
+        self.n_ctr = int(ctr.shape[0])
+        self.n_tgt = int(tgt.shape[0])
+        if near.n_ctr != self.n_ctr:
+            raise ValueError(f"near lists have {near.n_ctr} rows for {self.n_ctr} centers")
+        if int(tptr.shape[0]) != self.n_ctr + 1:
+            raise ValueError("tgt_ptr must have n_centers + 1 entries")
+        spec = cfg.spec
+        self.eq = _equation_code(spec)
+        self.variant = spec.variant_code
+        self.k = float(spec.helmholtz_k or 0.0)
+        self.with_normals = 1 if spec.needs_source_normals else 0
+        st = dv.stream_handle(dev)
+        nd = int(L.tsqbx_packed_doubles(self.n_src, self.with_normals))
+        self.packed = torch.empty(max(nd, 4), dtype=torch.float64, device=dev)
+        _lib.check(L.tsqbx_pack_sources(self.n_src, dv.ptr(src), dv.ptr(w),
+                                        dv.ptr(sn) if self.with_normals else None,
+                                        dv.ptr(near.src_perm), self.packed.data_ptr(), st),
+                   "tsqbx_pack_sources")
+        tn = tn if self.variant == 1 else None
+        if near.ctr_order is None:
+            self.ctr, self.tptr, self.tgt, self.tn, self.tidx = ctr, tptr, tgt, tn, None
+        else:
+            self.ctr = torch.empty_like(ctr)
+            self.tptr = torch.empty_like(tptr)
+            self.tgt = torch.empty_like(tgt)
+            self.tn = None if tn is None else torch.empty_like(tn)
+            self.tidx = torch.empty(max(self.n_tgt, 1), dtype=torch.int64, device=dev)
+            wsb = int(L.tsqbx_order_workspace_bytes(self.n_ctr))
+            ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+            _lib.check(L.tsqbx_order_targets(self.n_ctr, near.ctr_order.data_ptr(),
+                                             ctr.data_ptr(), tptr.data_ptr(), tgt.data_ptr(),
+                                             dv.ptr(tn), self.n_tgt, ws.data_ptr(), wsb,
+                                             self.ctr.data_ptr(), self.tptr.data_ptr(),
+                                             self.tgt.data_ptr(), dv.ptr(self.tn),
+                                             self.tidx.data_ptr(), st), "tsqbx_order_targets")
+        self.ws_bytes = int(L.tsqbx_eval_workspace_bytes(self.eq, self.variant, cfg.p_qbx,
+                                                         self.n_tgt))
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
+        self.err = torch.empty(1, dtype=torch.int64, device=dev)
+        self.G = int(group_lanes) if group_lanes else pick_group_lanes(near.mean_len)
+
+    def launch(self, out: torch.Tensor, validate: bool, generic: bool = False,
+               rows: tuple[int, int] | None = None, out_offset: int = 0,
+               user_order: bool = True) -> None:
+        """One evaluation launch.  ``rows=(g0, g1)`` restricts it to a row range
+        (multi-GPU shard); ``user_order=False`` writes processing order."""
+        L = _lib.load()
+        flags = (_lib.FLAG_VALIDATE if validate else 0) | (_lib.FLAG_GENERIC if generic else 0)
+        near = self.near
+        g0, g1 = rows if rows is not None else (0, self.n_ctr)
+        _lib.check(L.tsqbx_eval_packed(
+            self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,
+            self.with_normals, self.ctr.data_ptr() + 24 * g0, g1 - g0,
+            near.ptr.data_ptr() + 8 * g0, near.idx.data_ptr(), self.tgt.data_ptr(),
+            dv.ptr(self.tn), self.tptr.data_ptr() + 8 * g0, self.n_tgt,
+            dv.ptr(self.tidx) if user_order else None, out_offset, flags, self.G,
+            self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.err.data_ptr(),
+            dv.stream_handle(self.dev)), "tsqbx_eval_packed")
+
+    # --- validation -----------------------------------------------------------
+    def check_errors(self, batch_context: bool) -> None:
+        """Raise the reference's ValueError if the screened launch flagged a pair."""
+        if int(self.err.item()) == _lib.ERR_KEY_NONE:
+            return
+        L = _lib.load()
+        near = self.near
+        _lib.check(L.tsqbx_validate(self.packed.data_ptr(), self.n_src, self.ctr.data_ptr(),
+                                    self.n_ctr, near.ptr.data_ptr(), near.idx.data_ptr(),
+                                    self.tgt.data_ptr(), self.tptr.data_ptr(), self.n_tgt,
+                                    self.err.data_ptr(), dv.stream_handle(self.dev)),
+                   "tsqbx_validate")
+        key = int(self.err.item())
+        if key == _lib.ERR_KEY_NONE:
+            return            # screen tripped on non-finite weights, not on geometry
+        tp, kind, pos = key >> 32, (key >> 31) & 1, key & 0x7FFFFFFF
+        g = int(np.searchsorted(self.tptr.cpu().numpy(), tp, side="right") - 1)
+        ic = g if near.ctr_order is None else int(near.ctr_order[g].item())
+        it = tp if self.tidx is None else int(self.tidx[tp].item())
+        s_packed = int(near.idx[int(near.ptr[g].item()) + pos].item())
+        s_user = s_packed if near.src_perm is None else int(near.src_perm[s_packed].item())
+        where = (f" (target {it}, center {ic}, source index {s_user})" if batch_context else "")
+        if kind == 0:
+            raise ValueError(f"source {pos} coincides with the expansion center{where}")
+        c = self.user_ctr[ic].cpu().numpy()
+        s = self.src[s_user].cpu().numpy()
+        t = self.user_tgt[it].cpu().numpy()
+        R = float(np.linalg.norm(s - c))
+        r = float(np.linalg.norm(t - c))
+        raise ValueError(f"separation violation for source {pos}: |t-c| = {r} exceeds "
+                         f"|s-c| = {R}{where}")
+
+
+def _inputs(cfg, sources, weights, centers, targets, source_normals, target_normals, dev):
+    src = dv.to_device(sources, torch.float64, dev, (-1, 3))
+    if isinstance(weights, torch.Tensor) and not weights.is_complex():
+        weights = weights.to(torch.complex128)
+    w = dv.complex_as_f64(dv.to_device(weights, torch.complex128, dev, (-1,)))
+    if w.shape[0] != src.shape[0]:
+        raise ValueError("weights must have one entry per source")
+    ctr = dv.to_device(centers, torch.float64, dev, (-1, 3))
+    tgt = dv.to_device(targets, torch.float64, dev, (-1, 3))
+    sn = tn = None
+    if cfg.spec.needs_source_normals:
+        if source_normals is None:
+            raise ValueError("double-layer variant requires source normals")
+        sn = dv.to_device(source_normals, torch.float64, dev, (-1, 3))
+    if cfg.spec.needs_target_normals:
+        if target_normals is None:
+            raise ValueError("S' variant requires a target normal")
+        tn = dv.to_device(target_normals, torch.float64, dev, (-1, 3))
+    return src, w, ctr, tgt, sn, tn
+
+
+def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
+                        tgt_ptr=None, source_normals=None, target_normals=None,
+                        validate: bool = True, group_lanes: int | None = None, device=None):
+    """Per-target TSQBX potentials for many centers in one launch.
+
+    sources (n_src, 3), weights (n_src,) complex, centers (n_ctr, 3),
+    targets (n_tgt, 3) grouped by center: targets ``tgt_ptr[c]:tgt_ptr[c+1]``
+    belong to center c (default: one target per center).  ``near`` is a
+    :class:`NearLists` from :func:`build_near_lists` or a user CSR
+    ``(ptr, idx)`` with rows by center and indices into ``sources``.
+
+    Each target's value equals the reference's
+    ``ts_accumulate(cfg, sources[near(c)], weights[near(c)], centers[c], t)``
+    (tsqbx.py:68-80).  Returns complex128: numpy for host inputs, a CUDA
+    tensor when ``sources`` is a CUDA tensor.
+    """
+    host_out = not (isinstance(sources, torch.Tensor) and sources.is_cuda)
+    dev = dv.require_cuda(device)
+    src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, centers, targets,
+                                       source_normals, target_normals, dev)
+    n_ctr = int(ctr.shape[0])
+    if tgt_ptr is None:
+        if tgt.shape[0] != n_ctr:
+            raise ValueError("tgt_ptr is required unless there is one target per center")
+        tptr = torch.arange(n_ctr + 1, dtype=torch.int64, device=dev)
+    else:
+        tptr = dv.to_device(tgt_ptr, torch.int64, dev)
+    if not isinstance(near, NearLists):
+        nptr, nidx = near
+        near = NearLists.from_user_csr(nptr, nidx, int(src.shape[0]), dev)
+    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+    out = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
+    if prep.n_tgt:
+        prep.launch(torch.view_as_real(out), validate)
+        if validate:
+            prep.check_errors(batch_context=True)
+    return out.cpu().numpy() if host_out else out
+
+
+def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, targets,
+                          tgt_ptr=None, source_normals=None, target_normals=None,
+                          validate: bool = True, group_lanes: int | None = None, device=None):
+    """The whole near-field path in one call: geometry -> device radius-ball near
+    lists (``build_near_lists``) -> TSQBX evaluation -> per-target potentials.
+
+    Host inputs are copied to the device once; the result comes back as numpy
+    (or stays a CUDA tensor when ``sources`` is one)."""
+    from .nearlist import build_near_lists
+
+    host_out = not (isinstance(sources, torch.Tensor) and sources.is_cuda)
+    dev = dv.require_cuda(device)
+    src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, centers, targets, source_normals,
+                                       target_normals, dev)
+    n_ctr = int(ctr.shape[0])
+    rad = (near_radii.to(device=dev, dtype=torch.float64) if isinstance(near_radii, torch.Tensor)
+           else dv.to_device(np.broadcast_to(np.asarray(near_radii, np.float64), (n_ctr,)),
+                             torch.float64, dev))
+    tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
+            else dv.to_device(tgt_ptr, torch.int64, dev))
+    near = build_near_lists(ctr, src, rad, dev)
+    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+    out = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
+    if prep.n_tgt:
+        prep.launch(torch.view_as_real(out), validate)
+        if validate:
+            prep.check_errors(batch_context=True)
+    return out.cpu().numpy() if host_out else out
+
+
+class TsqbxProblem:
+    """A TSQBX problem resident in HBM: packed sources, CSR, targets, workspace.
+
+    ``evaluate()`` is one launch of the hot path over every (center, target);
+    nothing is copied between host and device.
+    """
+
+    def __init__(self, cfg: TsConfig, sources, weights, centers, targets, near: NearLists,
+                 tgt_ptr=None, source_normals=None, target_normals=None,
+                 group_lanes: int | None = None, device=None):
+        dev = dv.require_cuda(device)
+        src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, centers, targets,
+                                           source_normals, target_normals, dev)
+        n_ctr = int(ctr.shape[0])
+        tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
+                else dv.to_device(tgt_ptr, torch.int64, dev))
+        self.prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+        self.out = torch.empty(self.prep.n_tgt, dtype=torch.complex128, device=dev)
+        self.n_pairs_per_target = None
+
+    @property
+    def group_lanes(self) -> int:
+        return self.prep.G
+
+    def evaluate(self, validate: bool = False, generic: bool = False) -> torch.Tensor:
+        if self.prep.n_tgt:
+            self.prep.launch(torch.view_as_real(self.out), validate, generic)
+            if validate:
+                self.prep.check_errors(batch_context=True)
+        return self.out
+
+    def pair_count(self) -> int:
+        """Number of (target, near source) pairs one evaluate() processes."""
+        near, prep = self.prep.near, self.prep
+        lens = near.ptr[1:] - near.ptr[:-1]
+        tpc = prep.tptr[1:] - prep.tptr[:-1]
+        return int((lens * tpc).sum().item())
+
+
+def ts_accumulate(cfg: TsConfig, sources, weights, center, target,
+                  source_normals=None, target_normal=None) -> complex:
+    """sum_j w_j * (p-th order target-specific expansion of source j)  (tsqbx.py:68-80)."""
+    sources = np.ascontiguousarray(sources, dtype=np.float64).reshape(-1, 3)
+    weights = np.ascontiguousarray(weights, dtype=np.complex128).reshape(-1)
+    center = np.asarray(center, dtype=np.float64).reshape(1, 3)
+    target = np.asarray(target, dtype=np.float64).reshape(1, 3)
+    if cfg.spec.needs_source_normals and source_normals is None:
+        raise ValueError("double-layer variant requires source normals")
+    if cfg.spec.needs_target_normals and target_normal is None:
+        raise ValueError("S' variant requires a target normal")
+    n = sources.shape[0]
+    if n == 0:
+        return 0.0 + 0.0j
+    dev = dv.require_cuda()
+    src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, center, target, source_normals,
+                                       None if target_normal is None else
+                                       np.asarray(target_normal, dtype=np.float64).reshape(1, 3),
+                                       dev)
+    near = NearLists(n_ctr=1, n_src=n, n_pairs=n,
+                     ptr=torch.tensor([0, n], dtype=torch.int64, device=dev),
+                     idx=torch.arange(n, dtype=torch.int32, device=dev))
+    tptr = torch.tensor([0, 1], dtype=torch.int64, device=dev)
+    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr)
+    out = torch.empty(1, dtype=torch.complex128, device=dev)
+    prep.launch(torch.view_as_real(out), validate=True)
+    prep.check_errors(batch_context=False)
+    return complex(out.cpu().numpy()[0])
+
+
+def ts_eval(cfg: TsConfig, source, center, target, source_normal=None,
+            target_normal=None) -> complex:
+    """Target-specific expansion value for a single unit-weight source (tsqbx.py:83-92)."""
+    sn = None if source_normal is None else np.asarray(source_normal).reshape(1, 3)
+    return ts_accumulate(cfg, np.asarray(source, dtype=np.float64).reshape(1, 3),
+                         np.ones(1, dtype=np.complex128), center, target,
+                         source_normals=sn, target_normal=target_normal)

@@ -1,0 +1,142 @@
+"""Generate the golden vectors in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (needs /root/reference; never at test time):
+
+    python tests/golden/make_golden.py
+
+The reference package is imported read-only from /root/reference/pkg/src.
+Its backend selection falls back to the NumPy twin there (the compiled
+`_core` is not built in the read-only tree); the compiled Cython core built by
+`make -C oracle ref` (oracle/_ref/_core*.so) is called directly as well, so
+every vector is produced by both reference backends and they are checked to
+agree before saving.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import gigaqbx.tsqbx as rts  # noqa: E402
+from gigaqbx._backend import _ref as ref_numpy  # noqa: E402
+from gigaqbx.kernels import Equation, KernelSpec, Variant  # noqa: E402
+
+import oracle  # noqa: E402
+
+core = oracle.ref_core()
+assert core is not None, "build oracle/_ref first: make -C oracle ref"
+
+VARIANTS = [Variant.SINGLE_LAYER, Variant.TARGET_NORMAL_DERIV, Variant.SOURCE_NORMAL_DERIV]
+
+
+def unit(v):
+    return v / np.linalg.norm(v)
+
+
+def pair_cases():
+    """60 random admissible (s, c, t) per (equation, variant), p = 8, k = 2.2,
+    drawn like pkg/tests/test_tsqbx.py:19-25 (rho <= 0.9)."""
+    rng = np.random.default_rng(99)
+    rows = []
+    for eq, k in ((Equation.LAPLACE, None), (Equation.HELMHOLTZ, 2.2)):
+        for var in VARIANTS:
+            spec = KernelSpec(equation=eq, helmholtz_k=k, variant=var)
+            cfg = rts.TsConfig(spec, 8)
+            for _ in range(60):
+                c = rng.normal(size=3)
+                R = rng.uniform(0.5, 2.0)
+                s = c + R * unit(rng.normal(size=3))
+                r = rng.uniform(0.0, 0.9) * R
+                t = c + r * unit(rng.normal(size=3))
+                sn = unit(rng.normal(size=3))
+                tn = unit(rng.normal(size=3))
+                v = rts.ts_eval(cfg, s, c, t, source_normal=sn if spec.needs_source_normals
+                                else None, target_normal=tn if spec.needs_target_normals
+                                else None)
+                rows.append((0 if eq is Equation.LAPLACE else 1, spec.variant_code,
+                             k or 0.0, s, c, t, sn, tn, v))
+    return dict(equation=np.array([r[0] for r in rows]), variant=np.array([r[1] for r in rows]),
+                k=np.array([r[2] for r in rows]), p=np.array(8),
+                src=np.array([r[3] for r in rows]), ctr=np.array([r[4] for r in rows]),
+                tgt=np.array([r[5] for r in rows]), snrm=np.array([r[6] for r in rows]),
+                tnrm=np.array([r[7] for r in rows]), value=np.array([r[8] for r in rows]))
+
+
+def backend_batch():
+    """pkg/tests/test_backends.py:17-27,47-59 data: 40 sources at z~3, complex
+    weights, variants 0/1/2, target at / off center, p = 8, k = 1.7; values
+    from the compiled reference core (checked against the NumPy twin)."""
+    rng = np.random.default_rng(8)
+    src = rng.normal(size=(40, 3)) + np.array([0, 0, 3.0])
+    w = (rng.normal(size=40) + 1j * rng.normal(size=40)).astype(np.complex128)
+    sn = rng.normal(size=(40, 3))
+    sn /= np.linalg.norm(sn, axis=1)[:, None]
+    tn = np.array([0.0, 0.6, 0.8])
+    targets = np.array([[0.0, 0.0, 0.0], [0.05, 0.02, -0.03]])
+    lap = np.zeros((3, 2), complex)
+    hel = np.zeros((3, 2), complex)
+    c = np.zeros(3)
+    for v in range(3):
+        for it, t in enumerate(targets):
+            lap[v, it] = core.ts_accum_laplace(v, 8, src, w, sn, c, t, tn)
+            hel[v, it] = core.ts_accum_helmholtz(v, 1.7, 8, src, w, sn, c, t, tn)
+            a = ref_numpy.ts_accum_laplace(v, 8, src, w, sn, c, t, tn)
+            b = ref_numpy.ts_accum_helmholtz(v, 1.7, 8, src, w, sn, c, t, tn)
+            assert abs(a - lap[v, it]) <= 5e-13 * abs(a) and abs(b - hel[v, it]) <= 5e-13 * abs(b)
+    return dict(src=src, w=w, snrm=sn, tnrm=tn, targets=targets, p=np.array(8), k=np.array(1.7),
+                laplace=lap, helmholtz=hel)
+
+
+def sphere_case(n, p, k, mult, off_surface, seed):
+    """Fibonacci-sphere batch (BASELINE config geometry at size n) through the
+    reference's PUBLIC ts_accumulate, one call per (center, target)."""
+    from paper_1811_01110_b200 import configs
+    name = "c3" if k else ("c2" if off_surface else "c1")
+    case = configs.make_case(name, "literal", seed=seed, n=n)
+    ptr, idx = oracle.near_csr(case.centers, mult * case.expansion_radii, case.sources)
+    spec = case.cfg.spec
+    cfg = rts.TsConfig(rts.KernelSpec(equation=Equation(spec.equation.value),
+                                      variant=Variant(spec.variant.value),
+                                      helmholtz_k=spec.helmholtz_k), p)
+    out = np.zeros(case.n_targets, complex)
+    out_core = np.zeros(case.n_targets, complex)
+    for ic in range(case.n_centers):
+        sel = idx[ptr[ic]:ptr[ic + 1]]
+        for it in range(case.tgt_ptr[ic], case.tgt_ptr[ic + 1]):
+            out[it] = rts.ts_accumulate(cfg, case.sources[sel], case.weights[sel],
+                                        case.centers[ic], case.targets[it])
+            if k:
+                out_core[it] = core.ts_accum_helmholtz(0, k, p, np.ascontiguousarray(
+                    case.sources[sel]), np.ascontiguousarray(case.weights[sel]), None,
+                    case.centers[ic], case.targets[it], None)
+            else:
+                out_core[it] = core.ts_accum_laplace(0, p, np.ascontiguousarray(
+                    case.sources[sel]), np.ascontiguousarray(case.weights[sel]), None,
+                    case.centers[ic], case.targets[it], None)
+    err = np.max(np.abs(out - out_core)) / np.max(np.abs(out_core))
+    assert err < 1e-14, err
+    return dict(sources=case.sources, weights=case.weights, centers=case.centers,
+                targets=case.targets, tgt_ptr=case.tgt_ptr, near_ptr=ptr, near_idx=idx,
+                p=np.array(p), k=np.array(k or 0.0), value=out)
+
+
+def main():
+    np.savez_compressed(os.path.join(HERE, "pairs_p8.npz"), **pair_cases())
+    np.savez_compressed(os.path.join(HERE, "backend_batch.npz"), **backend_batch())
+    np.savez_compressed(os.path.join(HERE, "c1_literal.npz"),
+                        **sphere_case(4096, 4, None, 3.0, False, 0))
+    np.savez_compressed(os.path.join(HERE, "c2_small_literal.npz"),
+                        **sphere_case(2048, 8, None, 4.0, True, 1))
+    np.savez_compressed(os.path.join(HERE, "c3_small_literal.npz"),
+                        **sphere_case(2048, 8, 10.0, 4.0, True, 2))
+    for f in sorted(os.listdir(HERE)):
+        print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,343 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+Mirrors the reference's hot-path tests (pkg/tests/test_tsqbx.py,
+test_backends.py) plus config-level parity on the BASELINE geometries.
+Tolerances (north_star): normwise relative l-inf <= 1e-12 Laplace,
+<= 1e-10 Helmholtz; near-list membership bit-exact.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1811_01110_b200 import (KernelSpec, TsConfig, TsqbxProblem, build_near_lists,
+                                   get_backend, ts_accumulate, ts_accumulate_batch, ts_eval)
+from paper_1811_01110_b200 import configs
+from paper_1811_01110_b200.kernels import Equation, Variant
+
+pytestmark = pytest.mark.gpu
+
+LAP_TOL = 1e-12
+HELM_TOL = 1e-10
+VARIANTS = [Variant.SINGLE_LAYER, Variant.TARGET_NORMAL_DERIV, Variant.SOURCE_NORMAL_DERIV]
+
+
+def normwise(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
+
+
+def sorted_rows(ptr, idx):
+    return [np.sort(idx[ptr[i]:ptr[i + 1]]) for i in range(len(ptr) - 1)]
+
+
+# --- reference known answers (test_tsqbx.py) --------------------------------------
+def test_collinear_geometric_sum():
+    v = ts_eval(TsConfig(KernelSpec(), 2), [0, 0, 1.0], np.zeros(3), [0, 0, 0.5])
+    assert v == pytest.approx((1 + 0.5 + 0.25) / (4 * math.pi), rel=1e-14)
+    assert v == pytest.approx(0.139261, abs=1e-6)
+
+
+def test_target_at_center():
+    s = np.array([0.3, -0.4, 1.2])
+    v = ts_eval(TsConfig(KernelSpec(), 8), s, np.zeros(3), np.zeros(3))
+    assert v == pytest.approx(1.0 / (4 * math.pi * np.linalg.norm(s)), rel=1e-14)
+
+
+def test_separation_violation_raises():
+    with pytest.raises(ValueError, match="separation violation"):
+        ts_eval(TsConfig(KernelSpec(), 8), [0, 0, 1.0], np.zeros(3), [0, 1.1, 0])
+
+
+def test_singular_center_raises():
+    with pytest.raises(ValueError, match="coincides"):
+        ts_eval(TsConfig(KernelSpec(), 8), np.zeros(3), np.zeros(3), np.zeros(3))
+
+
+def test_separation_error_names_source_index():
+    src = np.array([[0, 0, 2.0], [0, 0, 0.4]])
+    with pytest.raises(ValueError, match="source 1"):
+        ts_accumulate(TsConfig(KernelSpec(), 8), src, np.ones(2), np.zeros(3), [0, 0.5, 0])
+
+
+def test_coincidence_outranks_separation():
+    src = np.array([[0, 0, 0.4], [0, 0, 0.0]])
+    with pytest.raises(ValueError, match="source 1 coincides"):
+        ts_accumulate(TsConfig(KernelSpec(), 8), src, np.ones(2), np.zeros(3), [0, 0.5, 0])
+
+
+def test_empty_batch_and_single_source():
+    cfg = TsConfig(KernelSpec(), 8)
+    assert ts_accumulate(cfg, np.zeros((0, 3)), np.zeros(0), np.zeros(3), np.zeros(3)) == 0.0
+    s, c, t = np.array([0.2, 0.9, -0.5]), np.array([0.1, 0.0, 0.0]), np.array([0.3, 0.1, 0.2])
+    a = ts_accumulate(cfg, s[None], np.array([1.3 - 0.4j]), c, t)
+    assert a == pytest.approx((1.3 - 0.4j) * ts_eval(cfg, s, c, t), rel=1e-14)
+
+
+def test_laplace_outputs_real():
+    v = ts_eval(TsConfig(KernelSpec(), 8), [0.2, 0.9, -0.5], [0.1, 0, 0], [0.3, 0.1, 0.2])
+    assert v.imag == 0.0
+
+
+def test_normals_required():
+    with pytest.raises(ValueError, match="source normals"):
+        ts_eval(TsConfig(KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV), 4), [0, 0, 1.0],
+                np.zeros(3), [0, 0, 0.1])
+    with pytest.raises(ValueError, match="target normal"):
+        ts_eval(TsConfig(KernelSpec(variant=Variant.TARGET_NORMAL_DERIV), 4), [0, 0, 1.0],
+                np.zeros(3), [0, 0, 0.1])
+
+
+# --- golden vectors produced by the reference ---------------------------------------
+def test_all_variants_match_reference_pairs(golden_dir):
+    """60 random admissible configs x (Laplace, Helmholtz) x (S, S', D), p = 8
+    (test_tsqbx.py:71-85), against the reference's own ts_eval values."""
+    g = np.load(os.path.join(golden_dir, "pairs_p8.npz"))
+    for i in range(g["value"].shape[0]):
+        eq, var, k = int(g["equation"][i]), int(g["variant"][i]), float(g["k"][i])
+        spec = KernelSpec(equation=Equation.LAPLACE if eq == 0 else Equation.HELMHOLTZ,
+                          variant=VARIANTS[var], helmholtz_k=None if eq == 0 else k)
+        a = ts_eval(TsConfig(spec, 8), g["src"][i], g["ctr"][i], g["tgt"][i],
+                    source_normal=g["snrm"][i] if var == 2 else None,
+                    target_normal=g["tnrm"][i] if var == 1 else None)
+        b = g["value"][i]
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(b)), (i, eq, var, a, b)
+
+
+def test_cuda_backend_matches_reference_backends(golden_dir):
+    """test_backends.py:47-59 on the cuda backend module."""
+    g = np.load(os.path.join(golden_dir, "backend_batch.npz"))
+    be = get_backend("cuda")
+    for v in range(3):
+        for it, t in enumerate(g["targets"]):
+            a = be.ts_accum_laplace(v, 8, g["src"], g["w"], g["snrm"], np.zeros(3), t, g["tnrm"])
+            b = be.ts_accum_helmholtz(v, 1.7, 8, g["src"], g["w"], g["snrm"], np.zeros(3), t,
+                                      g["tnrm"])
+            assert normwise(a, g["laplace"][v, it]) <= 5e-13
+            assert normwise(b, g["helmholtz"][v, it]) <= 5e-13
+
+
+@pytest.mark.parametrize("name,tol", [("c1_literal", LAP_TOL), ("c2_small_literal", LAP_TOL),
+                                      ("c3_small_literal", HELM_TOL)])
+def test_batch_matches_reference_golden(golden_dir, name, tol):
+    g = np.load(os.path.join(golden_dir, name + ".npz"))
+    k = float(g["k"])
+    spec = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=k) if k else KernelSpec()
+    cfg = TsConfig(spec, int(g["p"]))
+    out = ts_accumulate_batch(cfg, g["sources"], g["weights"], g["centers"], g["targets"],
+                              (g["near_ptr"], g["near_idx"]), tgt_ptr=g["tgt_ptr"])
+    assert normwise(out, g["value"]) <= tol
+    # same values through the device-built near lists
+    h = math.sqrt(4 * math.pi / g["sources"].shape[0])
+    mult = 3.0 if name.startswith("c1") else 4.0
+    near = build_near_lists(g["centers"], g["sources"], mult * 0.5 * h)
+    uptr, uidx = near.to_user_csr()
+    assert np.array_equal(uptr, g["near_ptr"])
+    assert all(np.array_equal(a, b) for a, b in zip(sorted_rows(uptr, uidx),
+                                                    sorted_rows(g["near_ptr"], g["near_idx"])))
+    out2 = ts_accumulate_batch(cfg, g["sources"], g["weights"], g["centers"], g["targets"], near,
+                               tgt_ptr=g["tgt_ptr"])
+    assert normwise(out2, g["value"]) <= tol
+
+
+# --- near-list builder vs oracle membership ------------------------------------------
+@pytest.mark.parametrize("name,preset", [("c1", "literal"), ("c1", "dense"), ("c2", "literal"),
+                                         ("c4", "literal"), ("c5", "literal")])
+def test_near_lists_bit_exact(name, preset):
+    kw = {"n": 65536, "spheres": 4} if name == "c5" else {}
+    case = configs.make_case(name, preset, **kw)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    uptr, uidx = near.to_user_csr()
+    optr, oidx = oracle.near_csr(case.centers, case.near_radii, case.sources)
+    assert near.n_pairs == len(oidx)
+    assert np.array_equal(uptr, optr)
+    srt = np.concatenate([np.sort(uidx[uptr[i]:uptr[i + 1]]) for i in range(case.n_centers)])
+    assert np.array_equal(srt, oidx)
+    # rows ascending in the packed (Morton) order
+    d = near.idx.cpu().numpy()
+    p = near.ptr.cpu().numpy()
+    inner = np.ones(len(d), bool)
+    inner[p[:-1][p[:-1] < len(d)]] = False
+    assert np.all(np.diff(d)[inner[1:]] > 0)
+
+
+def test_near_lists_edge_cases():
+    rng = np.random.default_rng(3)
+    src = rng.normal(size=(500, 3))
+    ctr = np.vstack([rng.normal(size=(50, 3)), [[100.0, 100.0, 100.0]]])   # last: no sources
+    rad = rng.uniform(0.0, 0.8, size=51)
+    rad[0] = 0.0                                                            # zero radius
+    near = build_near_lists(ctr, src, rad)
+    uptr, uidx = near.to_user_csr()
+    optr, oidx = oracle.near_csr(ctr, rad, src)
+    assert np.array_equal(uptr, optr) and uptr[-1] - uptr[-2] == 0
+    assert all(np.array_equal(a, b) for a, b in zip(sorted_rows(uptr, uidx),
+                                                    sorted_rows(optr, oidx)))
+    near0 = build_near_lists(ctr, np.zeros((0, 3)), rad)     # no sources at all
+    assert near0.n_pairs == 0
+    # duplicate points (ties) and a source exactly on the sphere of the radius
+    src2 = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 1.0], [0.0, 0.0, 1.0 + 1e-15], [0.5, 0, 0]])
+    near2 = build_near_lists(np.zeros((1, 3)), src2, 1.0)
+    u2p, u2i = near2.to_user_csr()
+    o2p, o2i = oracle.near_csr(np.zeros((1, 3)), [1.0], src2)
+    assert sorted(u2i.tolist()) == o2i.tolist()
+
+
+# --- config-level parity ------------------------------------------------------------
+def _case_parity(case, tol, subset=None, generic=False):
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr, source_normals=case.normals,
+                        target_normals=case.targets * 0 + case.normals[0])
+    out = prob.evaluate(validate=True, generic=generic).cpu().numpy()
+    uptr, uidx = near.to_user_csr()
+    spec = case.cfg.spec
+    eq = "laplace" if spec.is_laplace else "helmholtz"
+    if subset is None:
+        ref = oracle.ts_batch(eq, spec.variant_code, spec.helmholtz_k or 0.0, case.cfg.p_qbx,
+                              case.sources, case.weights, case.centers, uptr, uidx,
+                              case.targets, case.tgt_ptr)
+        err = normwise(out, ref)
+    else:
+        rng = np.random.default_rng(11)
+        sel = np.sort(rng.choice(case.n_centers, subset, replace=False))
+        lens = np.diff(uptr)[sel]
+        sptr = np.concatenate([[0], np.cumsum(lens)])
+        sidx = np.concatenate([uidx[uptr[c]:uptr[c + 1]] for c in sel])
+        tl = np.diff(case.tgt_ptr)[sel]
+        tptr = np.concatenate([[0], np.cumsum(tl)])
+        tsel = np.concatenate([np.arange(case.tgt_ptr[c], case.tgt_ptr[c + 1]) for c in sel])
+        ref = oracle.ts_batch(eq, spec.variant_code, spec.helmholtz_k or 0.0, case.cfg.p_qbx,
+                              case.sources, case.weights, case.centers[sel], sptr, sidx,
+                              case.targets[tsel], tptr)
+        err = normwise(out[tsel], ref)
+    assert err <= tol, err
+    return out, near
+
+
+@pytest.mark.parametrize("name,preset", [("c1", "literal"), ("c1", "dense")])
+def test_c1_full(name, preset):
+    _case_parity(configs.make_case(name, preset), LAP_TOL)
+
+
+@pytest.mark.parametrize("preset", ["literal", "dense"])
+def test_c2_c3_full_size_subset(preset):
+    _case_parity(configs.make_case("c2", preset), LAP_TOL, subset=4096)
+    _case_parity(configs.make_case("c3", preset), HELM_TOL, subset=4096)
+
+
+def test_c4_c5_subset():
+    _case_parity(configs.make_case("c4", "literal", n=262144), LAP_TOL, subset=4096)
+    _case_parity(configs.make_case("c4", "dense", n=65536), LAP_TOL, subset=2048)
+    _case_parity(configs.make_case("c5", "literal", n=65536, spheres=4), HELM_TOL, subset=4096)
+
+
+@pytest.mark.parametrize("p", list(range(0, 17)) + [20, 33])
+def test_order_sweep(p):
+    for name in ("c1", "c3"):
+        case = configs.make_case(name, "literal", n=2048)
+        case.cfg = TsConfig(case.cfg.spec, p)
+        _case_parity(case, LAP_TOL if name == "c1" else HELM_TOL)
+
+
+@pytest.mark.parametrize("eq,variant", [(e, v) for e in ("laplace", "helmholtz")
+                                        for v in VARIANTS])
+def test_variants_batch(eq, variant):
+    case = configs.make_case("c1" if eq == "laplace" else "c3", "literal", n=2048)
+    spec = KernelSpec(equation=Equation(eq), variant=variant,
+                      helmholtz_k=None if eq == "laplace" else 10.0)
+    case.cfg = TsConfig(spec, 8)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    tn = np.repeat(case.normals, np.diff(case.tgt_ptr), axis=0)
+    out = ts_accumulate_batch(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                              near, tgt_ptr=case.tgt_ptr, source_normals=case.normals,
+                              target_normals=tn)
+    uptr, uidx = near.to_user_csr()
+    ref = oracle.ts_batch(eq, spec.variant_code, spec.helmholtz_k or 0.0, 8, case.sources,
+                          case.weights, case.centers, uptr, uidx, case.targets, case.tgt_ptr,
+                          snormals=case.normals, tnormals=tn)
+    assert normwise(out, ref) <= (LAP_TOL if eq == "laplace" else HELM_TOL)
+
+
+def test_fast_and_generic_kernels_agree():
+    for name, tol in (("c2", LAP_TOL), ("c3", HELM_TOL)):
+        case = configs.make_case(name, "dense", n=16384)
+        a, _ = _case_parity(case, tol)
+        b, _ = _case_parity(case, tol, generic=True)
+        assert normwise(a, b) <= tol
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16, 32])
+def test_group_lanes_all_agree(G):
+    case = configs.make_case("c2", "dense", n=8192)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    uptr, uidx = near.to_user_csr()
+    ref = oracle.ts_batch("laplace", 0, 0.0, 8, case.sources, case.weights, case.centers, uptr,
+                          uidx, case.targets, case.tgt_ptr)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr, group_lanes=G)
+    assert normwise(prob.evaluate().cpu().numpy(), ref) <= LAP_TOL
+
+
+def test_ragged_targets_and_empty_rows():
+    rng = np.random.default_rng(7)
+    src = rng.normal(size=(300, 3)) * 0.5 + np.array([0, 0, 3.0])
+    ctr = rng.normal(size=(40, 3)) * 0.1
+    ntg = rng.integers(0, 4, size=40)                      # 0..3 targets per center
+    tptr = np.concatenate([[0], np.cumsum(ntg)])
+    tgt = np.repeat(ctr, ntg, axis=0) + rng.normal(size=(tptr[-1], 3)) * 0.05
+    lens = rng.integers(0, 30, size=40)
+    lens[::5] = 0                                          # empty rows
+    nptr = np.concatenate([[0], np.cumsum(lens)])
+    nidx = rng.integers(0, 300, size=nptr[-1]).astype(np.int32)
+    w = rng.normal(size=300) + 1j * rng.normal(size=300)
+    for spec, tol in ((KernelSpec(), LAP_TOL),
+                      (KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=3.0), HELM_TOL)):
+        cfg = TsConfig(spec, 8)
+        out = ts_accumulate_batch(cfg, src, w, ctr, tgt, (nptr, nidx), tgt_ptr=tptr)
+        ref = oracle.ts_batch("laplace" if spec.is_laplace else "helmholtz", 0,
+                              spec.helmholtz_k or 0.0, 8, src, w, ctr, nptr, nidx, tgt, tptr)
+        assert normwise(out, ref) <= tol
+        for ic in np.nonzero(lens == 0)[0]:
+            assert np.all(out[tptr[ic]:tptr[ic + 1]] == 0)
+
+
+def test_batch_validation_names_target_and_source():
+    case = configs.make_case("c1", "literal", n=1024)
+    tg = case.targets.copy()
+    tg[37] = case.centers[37] + 10.0 * case.expansion_radii[37]     # far outside: violation
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    with pytest.raises(ValueError, match=r"separation violation for source \d+: .*target 37"):
+        ts_accumulate_batch(case.cfg, case.sources, case.weights, case.centers, tg, near)
+    out = ts_accumulate_batch(case.cfg, case.sources, case.weights, case.centers, tg, near,
+                              validate=False)
+    assert out.shape == (1024,)
+
+
+def test_full_size_properties_c2_dense():
+    """At BASELINE size: linearity in the weights and invariance under a
+    permutation of the source order (size-independent properties)."""
+    case = configs.make_case("c2", "dense")
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    p1 = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                      tgt_ptr=case.tgt_ptr)
+    u1 = p1.evaluate().clone()
+    w2 = np.random.default_rng(4).normal(size=case.n_sources) + 0j
+    p2 = TsqbxProblem(case.cfg, case.sources, w2, case.centers, case.targets, near,
+                      tgt_ptr=case.tgt_ptr)
+    u2 = p2.evaluate().clone()
+    p3 = TsqbxProblem(case.cfg, case.sources, case.weights + 2.0 * w2, case.centers,
+                      case.targets, near, tgt_ptr=case.tgt_ptr)
+    u3 = p3.evaluate().clone()
+    assert normwise((u1 + 2 * u2).cpu().numpy(), u3.cpu().numpy()) <= 1e-12
+    perm = np.random.default_rng(5).permutation(case.n_sources)
+    near_p = build_near_lists(case.centers, case.sources[perm], case.near_radii)
+    assert near_p.n_pairs == near.n_pairs
+    p4 = TsqbxProblem(case.cfg, case.sources[perm], case.weights[perm], case.centers,
+                      case.targets, near_p, tgt_ptr=case.tgt_ptr)
+    assert normwise(p4.evaluate().cpu().numpy(), u1.cpu().numpy()) <= 1e-13
+    assert np.all(np.isfinite(u1.cpu().numpy()))
