@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 1
+#define TSQBX_ABI_VERSION 2
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -52,6 +52,7 @@ extern "C" {
 
 #define TSQBX_FLAG_VALIDATE 1u   /* cheap in-kernel screening, see tsqbx_validate */
 #define TSQBX_FLAG_GENERIC 2u    /* force the runtime-p reference-order kernel */
+#define TSQBX_FLAG_REAL_WEIGHTS 4u /* caller guarantees Im w == 0: skip the imaginary part */
 
 #define TSQBX_MAX_ORDER 64
 
@@ -82,6 +83,9 @@ int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const 
  *   ctr_xyz     : n_ctr x 3 centers, row g
  *   near_ptr    : n_ctr + 1 row offsets into near_idx
  *   near_idx    : source indices into `packed`
+ *   sell_ptr/idx: optional sliced-ELL copy of the same lists (tsqbx_sell_build);
+ *                 when given, the thread-per-center kernels run on it (row ranges
+ *                 must then start at a multiple of 32)
  *   tgt_xyz     : n_tgt x 3 targets grouped by row: the targets of row g are
  *                 tgt_ptr[g] .. tgt_ptr[g+1]-1
  *   tgt_nrm     : n_tgt x 3 (S' only, else NULL)
@@ -99,6 +103,7 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p,
                       const double* packed, int64_t n_src, int with_normals,
                       const double* ctr_xyz, int64_t n_ctr,
                       const int64_t* near_ptr, const int32_t* near_idx,
+                      const int64_t* sell_ptr, const int32_t* sell_idx,
                       const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
                       int64_t n_tgt, const int64_t* tgt_out, int64_t out_offset,
                       unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
@@ -171,6 +176,19 @@ int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* c
                         int64_t n_tgt, void* workspace, int64_t ws_bytes,
                         double* ctr_out, int64_t* tptr_out, double* tgt_out, double* tnrm_out,
                         int64_t* tgt_index, void* stream);
+
+/* Sliced-ELL (SELL-32x4) copy of a CSR: rows in slices of 32; a slice's width
+ * is its longest row rounded up to 4, and entry (row r, column i) sits at
+ * sell_ptr[r/32] + (i/4)*128 + (r%32)*4 + i%4 -- column blocks of 4 so that a
+ * lane fetches 4 upcoming indices with one 16-byte load and a warp one 512-byte
+ * run.  sell_ptr has ceil(n_rows/32) + 1 offsets (multiples of 128),
+ * *n_entries (device) the total.
+ * Two phases like the near lists: tsqbx_sell_size then tsqbx_sell_fill. */
+int64_t tsqbx_sell_workspace_bytes(int64_t n_rows);
+int tsqbx_sell_size(int64_t n_rows, const int64_t* near_ptr, void* workspace, int64_t ws_bytes,
+                    int64_t* sell_ptr, int64_t* n_entries, void* stream);
+int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near_idx,
+                    const int64_t* sell_ptr, int32_t* sell_idx, void* stream);
 
 /* out[dest[i]] = src[i] for n complex128 values (dest NULL = copy); assembles
  * all-gathered shards into user target order. */

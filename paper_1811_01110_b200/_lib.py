@@ -28,6 +28,7 @@ EQ_LAPLACE = 0
 EQ_HELMHOLTZ = 1
 FLAG_VALIDATE = 1
 FLAG_GENERIC = 2
+FLAG_REAL_WEIGHTS = 4
 MAX_ORDER = 64
 ERR_KEY_NONE = (1 << 63) - 1
 ERR_KEY_SUSPECT = (1 << 63) - 2
@@ -46,8 +47,8 @@ SIGNATURES = {
     "tsqbx_packed_doubles": (_I64, [_I64, _I]),
     "tsqbx_pack_sources": (_I, [_I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_eval_workspace_bytes": (_I64, [_I, _I, _I, _I64]),
-    "tsqbx_eval_packed": (_I, [_I, _I, _D, _I, _P, _I64, _I, _P, _I64, _P, _P, _P, _P, _P,
-                               _I64, _P, _I64, _U, _I, _P, _I64, _P, _P, _P]),
+    "tsqbx_eval_packed": (_I, [_I, _I, _D, _I, _P, _I64, _I, _P, _I64, _P, _P, _P, _P, _P, _P,
+                               _P, _I64, _P, _I64, _U, _I, _P, _I64, _P, _P, _P]),
     "tsqbx_user_workspace_bytes": (_I64, [_I, _I, _I, _I64, _I64]),
     "tsqbx_eval_laplace": (_I, [_I, _I, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64, _U,
                                 _P, _I64, _P, _P, _P]),
@@ -58,6 +59,9 @@ SIGNATURES = {
     "tsqbx_order_targets": (_I, [_I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P,
                                  _P]),
     "tsqbx_scatter_c128": (_I, [_I64, _P, _P, _P, _P]),
+    "tsqbx_sell_workspace_bytes": (_I64, [_I64]),
+    "tsqbx_sell_size": (_I, [_I64, _P, _P, _I64, _P, _P, _P]),
+    "tsqbx_sell_fill": (_I, [_I64, _P, _P, _P, _P, _P]),
     "tsqbx_near_workspace_bytes": (_I64, [_I64, _I64]),
     "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
     "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P]),
@@ -94,7 +98,7 @@ def load():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.tsqbx_abi_version() != 1:
+        if L.tsqbx_abi_version() != 2:
             raise RuntimeError("TSQBX ABI version mismatch")
         _lib = L
     return _lib

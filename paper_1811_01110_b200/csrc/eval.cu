@@ -46,6 +46,8 @@ struct EvalParams {
   const double* __restrict__ ctr;    // processing order
   const int64_t* __restrict__ nptr;
   const int32_t* __restrict__ nidx;
+  const int64_t* __restrict__ sell_ptr;  // sliced-ELL layout (null = CSR only)
+  const int32_t* __restrict__ sell_idx;
   const double* __restrict__ tgt;
   const double* __restrict__ tnrm;
   const int64_t* __restrict__ tptr;  // rows in processing order
@@ -59,7 +61,9 @@ struct EvalParams {
   int p;
   int variant;
   int G;
+  int log2G;
   int validate;
+  int real_w;
   double k;
 };
 
@@ -72,20 +76,83 @@ __device__ __forceinline__ void flag_suspect(unsigned long long* err) {
 }
 
 // ---------------------------------------------------------------------------
+// Source stream of one CSR row for one lane: the row's entries j = lane,
+// lane + G, ... are read through a two-deep software pipeline (index two
+// iterations ahead, source record one iteration ahead) so the gather latency
+// overlaps the previous source's arithmetic.
+// ---------------------------------------------------------------------------
+struct SourceStream {
+  const int32_t* __restrict__ idx;   // this lane's first index entry
+  const double4* __restrict__ sp;
+  const double* __restrict__ swi;
+  int stride, count, i;
+  int s_next2;
+  double4 q_next;
+  double w_next;
+  bool real_w;
+
+  __device__ __forceinline__ SourceStream(const int32_t* first, int str, int n, const double4* p,
+                                          const double* wi, bool realw)
+      : idx(first), sp(p), swi(wi), stride(str), count(n), i(0), s_next2(0), w_next(0.0),
+        real_w(realw) {
+    q_next = make_double4(0.0, 0.0, 0.0, 0.0);
+    int s0 = 0;
+    if (count > 0) s0 = __ldg(idx);
+    if (count > 1) s_next2 = __ldg(idx + stride);
+    if (count > 0) {
+      q_next = ld256(sp + s0);
+      if (!real_w) w_next = __ldg(swi + s0);
+    }
+  }
+  __device__ __forceinline__ bool more() const { return i < count; }
+  // returns the current source and advances the pipeline
+  __device__ __forceinline__ void next(double4& q, double& wi) {
+    q = q_next;
+    wi = w_next;
+    if (i + 1 < count) {
+      q_next = ld256(sp + s_next2);
+      if (!real_w) w_next = __ldg(swi + s_next2);
+    }
+    if (i + 2 < count) s_next2 = __ldg(idx + (i + 2) * stride);
+    ++i;
+  }
+};
+
+// entries j = lane, lane + G, ... of a CSR row of length len
+__device__ __forceinline__ SourceStream csr_stream(const EvalParams& a, int64_t b, int len,
+                                                   int lane, int G) {
+  const int n = len > lane ? (len - lane + G - 1) / G : 0;
+  return SourceStream(a.nidx + b + lane, G, n, a.sp, a.swi, false);
+}
+
+struct GroupCoord {
+  int64_t g;
+  int lane, G;
+  unsigned mask;
+};
+
+__device__ __forceinline__ bool group_coord(const EvalParams& a, GroupCoord& c) {
+  const int lg = a.log2G;
+  c.G = 1 << lg;
+  c.g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> lg;
+  c.lane = (int)(threadIdx.x & (unsigned)(c.G - 1));
+  c.mask = group_mask(c.G);
+  return c.g < a.n_ctr;
+}
+
+// ---------------------------------------------------------------------------
 // Laplace S, compile-time order P, NT targets per pass.
 // Per pair: s-c, R^2, 1/R shared by the targets; per target A = (s-c).(t-c)/R^2,
 // B = |t-c|^2/R^2 and the 3-op/order Clenshaw series (common.cuh).
 // ---------------------------------------------------------------------------
 template <int P, int NT, bool VAL>
 __global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
-  const int G = a.G;
-  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t g = gt / G;
-  if (g >= a.n_ctr) return;
-  const int lane = (int)(threadIdx.x & (unsigned)(G - 1));
-  const unsigned mask = group_mask(G);
+  GroupCoord gc;
+  if (!group_coord(a, gc)) return;
+  const int64_t g = gc.g;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
-  const int64_t b = a.nptr[g], e = a.nptr[g + 1];
+  const int64_t b = a.nptr[g];
+  const int len = (int)(a.nptr[g + 1] - b);
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
 
   for (int64_t tb = t0; tb < t1; tb += NT) {
@@ -99,13 +166,14 @@ __global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
       r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
       ar[q] = ai[q] = bm[q] = 0.0;
     }
-    for (int64_t j = b + lane; j < e; j += G) {
-      const int s = __ldg(a.nidx + j);
-      const double4 q4 = ld256(a.sp + s);
-      const double wim = __ldg(a.swi + s);
+    SourceStream ss = csr_stream(a, b, len, gc.lane, gc.G);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
       const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const double iR = rsqrt(R2);
+      const double iR = rsqrt_fast(R2);
       const double iR2 = iR * iR;
       const double wr = q4.w * iR, wi = wim * iR;
 #pragma unroll
@@ -120,11 +188,11 @@ __global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
     }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      ar[q] = group_sum(ar[q], G, mask);
-      ai[q] = group_sum(ai[q], G, mask);
-      if (VAL) bm[q] = group_max(bm[q], G, mask);
+      ar[q] = group_sum(ar[q], gc.G, gc.mask);
+      ai[q] = group_sum(ai[q], gc.G, gc.mask);
+      if (VAL) bm[q] = group_max(bm[q], gc.G, gc.mask);
     }
-    if (lane == 0) {
+    if (gc.lane == 0) {
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         if (tb + q < t1) {
@@ -144,15 +212,12 @@ __global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
 // ---------------------------------------------------------------------------
 template <int P, int NT, bool VAL>
 __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
-  constexpr LegendreScale<P> L{};
-  const int G = a.G;
-  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t g = gt / G;
-  if (g >= a.n_ctr) return;
-  const int lane = (int)(threadIdx.x & (unsigned)(G - 1));
-  const unsigned mask = group_mask(G);
+  GroupCoord gc;
+  if (!group_coord(a, gc)) return;
+  const int64_t g = gc.g;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
-  const int64_t b = a.nptr[g], e = a.nptr[g + 1];
+  const int64_t b = a.nptr[g];
+  const int len = (int)(a.nptr[g + 1] - b);
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
 
@@ -174,13 +239,14 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
         cf[q][n] = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
       ar[q] = ai[q] = bm[q] = 0.0;
     }
-    for (int64_t j = b + lane; j < e; j += G) {
-      const int s = __ldg(a.nidx + j);
-      const double4 q4 = ld256(a.sp + s);
-      const double wim = __ldg(a.swi + s);
+    SourceStream ss = csr_stream(a, b, len, gc.lane, gc.G);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
       const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const double iR = rsqrt(R2);
+      const double iR = rsqrt_fast(R2);
       const double x = k * (R2 * iR);
       const double invx = iR * invk;
       double hr[P + 1], hi[P + 1];
@@ -209,7 +275,7 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
           si = fma(c1, hi[1], si);
 #pragma unroll
           for (int n = 1; n < P; ++n) {
-            const double pn = fma(L.alpha[n] * cg, pc, -pm);
+            const double pn = fma(c_leg.alpha[n] * cg, pc, -pm);
             pm = pc;
             pc = pn;
             const double cn = cf[q][n + 1] * pc;
@@ -224,19 +290,232 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
     }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      ar[q] = group_sum(ar[q], G, mask);
-      ai[q] = group_sum(ai[q], G, mask);
-      if (VAL) bm[q] = group_max(bm[q], G, mask);
+      ar[q] = group_sum(ar[q], gc.G, gc.mask);
+      ai[q] = group_sum(ai[q], gc.G, gc.mask);
+      if (VAL) bm[q] = group_max(bm[q], gc.G, gc.mask);
     }
-    if (lane == 0) {
+    if (gc.lane == 0) {
       const double pk = k * kInvFourPi;
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         if (tb + q < t1) {
-          a.out[out_slot(a, tb + q)] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) * acc
+          a.out[out_slot(a, tb + q)] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
           if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
             flag_suspect(a.err);
         }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Thread-per-center kernels on the sliced-ELL layout (SELL-32x4): rows are cut
+// into slices of 32 consecutive (Morton-adjacent) centers, and a slice's near
+// indices are stored in column blocks of 4, so lane l of a warp owns row 32s + l
+// and one 16-byte load per lane (512 coalesced bytes per warp) brings the next
+// 4 indices.  No shuffles, no reductions: each thread accumulates its own
+// center's targets.
+// ---------------------------------------------------------------------------
+// Source stream over one SELL-32x4 row.  The index stream (compulsory HBM
+// traffic) is staged through a per-thread shared-memory ring with cp.async:
+// kRing index blocks (4 entries each) are in flight ahead of use, so the
+// DRAM latency of the CSR stream never reaches the arithmetic.  The source
+// record (an L1/L2 gather) is fetched one entry ahead into registers.
+constexpr int kSellBlock = 128;   // threads per CTA of the SELL kernels
+constexpr int kRing = 4;          // index blocks in flight (16 entries of lookahead)
+
+struct SellStream {
+  const int4* __restrict__ blk;   // this lane's block 0; block b at blk + 32 b
+  const double4* __restrict__ sp;
+  const double* __restrict__ swi;
+  int4* ring;                     // [kRing + 1][kSellBlock] int4, this thread's column
+  int count, nblk, i;
+  int4 cur;                       // indices of block i / 4
+  double4 q_next;
+  double w_next;
+  bool real_w;
+
+  __device__ __forceinline__ void issue(int b) {
+    // block b goes to slot b % (kRing + 1); always commit so group counts stay uniform
+    if (b < nblk) cp_async16(ring + (b % (kRing + 1)) * kSellBlock, blk + 32 * b);
+    cp_async_commit();
+  }
+  __device__ __forceinline__ SellStream(const EvalParams& a, int64_t g, int n, bool realw,
+                                        int4* ring_base)
+      : sp(a.sp), swi(a.swi), count(n), i(0), w_next(0.0), real_w(realw) {
+    blk = reinterpret_cast<const int4*>(a.sell_idx + a.sell_ptr[g >> 5]) + (g & 31);
+    ring = ring_base + threadIdx.x;
+    nblk = (count + 3) >> 2;
+    q_next = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+    for (int b = 0; b < kRing; ++b) issue(b);
+    cur = make_int4(0, 0, 0, 0);
+    if (count > 0) enter_block(0);
+    if (count > 0) fetch(cur.x);
+  }
+  __device__ __forceinline__ void enter_block(int b) {
+    cp_async_wait<kRing - 1>();                 // block b has landed
+    cur = ring[(b % (kRing + 1)) * kSellBlock];
+    issue(b + kRing);                           // reuses the slot of block b - 1
+  }
+  __device__ __forceinline__ void fetch(int s) {
+    q_next = ld256(sp + s);
+    if (!real_w) w_next = __ldg(swi + s);
+  }
+  __device__ __forceinline__ bool more() const { return i < count; }
+  __device__ __forceinline__ void next(double4& q, double& wi) {
+    q = q_next;
+    wi = w_next;
+    ++i;
+    if (i < count) {
+      const int e = i & 3;
+      if (e == 0) enter_block(i >> 2);
+      fetch(e == 0 ? cur.x : e == 1 ? cur.y : e == 2 ? cur.z : cur.w);
+    }
+  }
+};
+
+template <int P, int NT, bool VAL, bool REALW>
+__global__ void __launch_bounds__(kSellBlock) laplace_sell_kernel(const EvalParams a) {
+  __shared__ int4 ring[(kRing + 1) * kSellBlock];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.n_ctr) return;
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      tx[q] = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    SellStream ss(a, g, len, REALW, ring);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt_fast(R2);
+      const double iR2 = iR * iR;
+      const double wr = q4.w * iR;
+      const double wi = REALW ? 0.0 : wim * iR;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const double A = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR2;
+        const double B = r2[q] * iR2;
+        const double S = laplace_series<P>(A, B);
+        ar[q] = fma(S, wr, ar[q]);
+        if (!REALW) ai[q] = fma(S, wi, ai[q]);
+        if (VAL) bm[q] = fmax(bm[q], B);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      if (tb + q < t1) {
+        a.out[out_slot(a, tb + q)] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
+        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+          flag_suspect(a.err);
+      }
+    }
+  }
+}
+
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalParams a) {
+  // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n live in shared
+  // memory ([n][q][thread], conflict-free) instead of 2(P+1) registers per target
+  __shared__ double cfs[(P + 1) * NT * kSellBlock];
+  __shared__ int4 ring[(kRing + 1) * kSellBlock];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.n_ctr) return;
+  const int tid = threadIdx.x;
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      const double ux = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      const double uy = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      const double uz = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(uz, uz, fma(uy, uy, ux * ux));
+      const double ir = r2[q] > 0.0 ? rsqrt(r2[q]) : 0.0;  // r = 0: cos g irrelevant
+      tx[q] = ux * ir;
+      ty[q] = uy * ir;
+      tz[q] = uz * ir;
+#pragma unroll
+      for (int n = 0; n <= P; ++n)
+        cfs[(n * NT + q) * kSellBlock + tid] = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    SellStream ss(a, g, len, false, ring);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt_fast(R2);
+      const double invx = iR * invk;
+      double hmr, hmi, hcr, hci;                 // h_{n-1}, h_n
+      hankel01(k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
+      double cg[NT], pm[NT], pc[NT], sr[NT], si[NT];
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        cg[q] = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
+        const double c0 = cfs[q * kSellBlock + tid];
+        sr[q] = c0 * hmr;
+        si[q] = c0 * hmi;
+        if constexpr (P >= 1) {
+          const double c1 = cfs[(NT + q) * kSellBlock + tid] * cg[q];
+          sr[q] = fma(c1, hcr, sr[q]);
+          si[q] = fma(c1, hci, si[q]);
+        }
+        pm[q] = 1.0;
+        pc[q] = cg[q];
+      }
+#pragma unroll
+      for (int n = 1; n < P; ++n) {
+        // h_{n+1} = (2n+1)/x h_n - h_{n-1}   (_core.pyx:192-193)
+        const double f = (2.0 * n + 1.0) * invx;
+        const double hnr = fma(f, hcr, -hmr), hni = fma(f, hci, -hmi);
+        hmr = hcr;
+        hmi = hci;
+        hcr = hnr;
+        hci = hni;
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          const double pn = fma(c_leg.alpha[n] * cg[q], pc[q], -pm[q]);
+          pm[q] = pc[q];
+          pc[q] = pn;
+          const double c = cfs[((n + 1) * NT + q) * kSellBlock + tid] * pn;
+          sr[q] = fma(c, hnr, sr[q]);
+          si[q] = fma(c, hni, si[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        ar[q] = fma(q4.w, sr[q], fma(-wim, si[q], ar[q]));
+        ai[q] = fma(q4.w, si[q], fma(wim, sr[q], ai[q]));
+        if (VAL) bm[q] = fmax(bm[q], r2[q] * (iR * iR));
+      }
+    }
+    const double pk = k * kInvFourPi;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      if (tb + q < t1) {
+        a.out[out_slot(a, tb + q)] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
+        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+          flag_suspect(a.err);
       }
     }
   }
@@ -535,7 +814,18 @@ __global__ void pack_kernel(int64_t n, const double* __restrict__ xyz,
 constexpr int kMaxFastOrder = 16;
 
 template <int P, int NT, bool VAL>
-void launch_fast(int equation, const EvalParams& a, int blocks, cudaStream_t st) {
+void launch_fast(int equation, bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
+  if (sell) {
+    const int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
+    if (equation == TSQBX_EQ_LAPLACE) {
+      if (a.real_w) laplace_sell_kernel<P, NT, VAL, true><<<blocks, kSellBlock, 0, st>>>(a);
+      else laplace_sell_kernel<P, NT, VAL, false><<<blocks, kSellBlock, 0, st>>>(a);
+    } else {
+      helmholtz_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
+    }
+    return;
+  }
+  const int blocks = (int)((n_ctr * a.G + 255) / 256);
   if (equation == TSQBX_EQ_LAPLACE)
     laplace_s_kernel<P, NT, VAL><<<blocks, 256, 0, st>>>(a);
   else
@@ -543,23 +833,24 @@ void launch_fast(int equation, const EvalParams& a, int blocks, cudaStream_t st)
 }
 
 template <int P>
-void launch_fast_p(int equation, int nt, bool val, const EvalParams& a, int blocks,
+void launch_fast_p(int equation, bool sell, int nt, bool val, const EvalParams& a, int64_t n_ctr,
                    cudaStream_t st) {
   if (nt >= 2) {
-    if (val) launch_fast<P, 2, true>(equation, a, blocks, st);
-    else launch_fast<P, 2, false>(equation, a, blocks, st);
+    if (val) launch_fast<P, 2, true>(equation, sell, a, n_ctr, st);
+    else launch_fast<P, 2, false>(equation, sell, a, n_ctr, st);
   } else {
-    if (val) launch_fast<P, 1, true>(equation, a, blocks, st);
-    else launch_fast<P, 1, false>(equation, a, blocks, st);
+    if (val) launch_fast<P, 1, true>(equation, sell, a, n_ctr, st);
+    else launch_fast<P, 1, false>(equation, sell, a, n_ctr, st);
   }
 }
 
 template <int... Ps>
 struct FastTable {
-  static bool run(int p, int equation, int nt, bool val, const EvalParams& a, int blocks,
-                  cudaStream_t st) {
+  static bool run(int p, int equation, bool sell, int nt, bool val, const EvalParams& a,
+                  int64_t n_ctr, cudaStream_t st) {
     bool done = false;
-    ((p == Ps ? (launch_fast_p<Ps>(equation, nt, val, a, blocks, st), done = true) : false), ...);
+    ((p == Ps ? (launch_fast_p<Ps>(equation, sell, nt, val, a, n_ctr, st), done = true) : false),
+     ...);
     return done;
   }
 };
@@ -610,14 +901,16 @@ int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const 
 }
 
 int64_t tsqbx_eval_workspace_bytes(int equation, int variant, int p, int64_t n_tgt) {
+  (void)variant;
   if (equation != TSQBX_EQ_HELMHOLTZ) return 0;
-  const int stride = (variant == 0 && p <= kMaxFastOrder) ? p + 1 : 2 * (p + 1);
-  return n_tgt * stride * (int64_t)sizeof(double) + 256;
+  // sized for the generic kernel's (j_n, j'_n) table so any flag combination fits
+  return n_tgt * 2 * (p + 1) * (int64_t)sizeof(double) + 256;
 }
 
 int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* packed,
                       int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
-                      const int64_t* near_ptr, const int32_t* near_idx, const double* tgt_xyz,
+                      const int64_t* near_ptr, const int32_t* near_idx,
+                      const int64_t* sell_ptr, const int32_t* sell_idx, const double* tgt_xyz,
                       const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
                       const int64_t* tgt_out, int64_t out_offset, unsigned flags,
                       int group_lanes, void* workspace, int64_t ws_bytes, double* out,
@@ -640,6 +933,8 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   if (n_src > INT32_MAX) return set_error(TSQBX_ERR_ARGUMENT, "n_src exceeds int32 indexing");
   if (n_ctr > 0 && (!ctr_xyz || !near_ptr || !tgt_ptr || !out || (n_tgt > 0 && !tgt_xyz)))
     return set_error(TSQBX_ERR_ARGUMENT, "null array");
+  if ((sell_ptr == nullptr) != (sell_idx == nullptr))
+    return set_error(TSQBX_ERR_ARGUMENT, "sell_ptr and sell_idx go together");
   int G = group_lanes <= 0 ? 8 : group_lanes;
   if (G > 32 || (G & (G - 1))) return set_error(TSQBX_ERR_ARGUMENT, "group_lanes must be 1..32, pow2");
   if (val) set_key<<<1, 1, 0, st>>>((unsigned long long*)err_key, (unsigned long long)TSQBX_ERR_KEY_NONE);
@@ -654,6 +949,9 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   a.ctr = ctr_xyz;
   a.nptr = near_ptr;
   a.nidx = near_idx;
+  a.sell_ptr = sell_ptr;
+  a.sell_idx = sell_idx;
+  a.real_w = (flags & TSQBX_FLAG_REAL_WEIGHTS) ? 1 : 0;
   a.tgt = tgt_xyz;
   a.tnrm = tgt_nrm;
   a.tptr = tgt_ptr;
@@ -665,6 +963,7 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   a.p = p;
   a.variant = variant;
   a.G = G;
+  a.log2G = __builtin_ctz((unsigned)G);
   a.validate = val ? 1 : 0;
   a.k = k;
   if (equation == TSQBX_EQ_HELMHOLTZ) {
@@ -679,8 +978,7 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   }
   if (fast) {
     const int nt = n_tgt >= 2 * n_ctr ? 2 : 1;
-    const int blocks = (int)((n_ctr * G + 255) / 256);
-    FastOrders::run(p, equation, nt, val, a, blocks, st);
+    FastOrders::run(p, equation, sell_ptr != nullptr, nt, val, a, n_ctr, st);
   } else {
     const int blocks = (int)((n_ctr * G + 127) / 128);
     generic_kernel<<<blocks, 128, 0, st>>>(a, equation);
@@ -712,7 +1010,8 @@ static int eval_user(int equation, int variant, double k, int p, const double* s
                               packed, stream);
   if (rc) return rc;
   return tsqbx_eval_packed(equation, variant, k, p, packed, n_src, variant == 2, ctr_xyz, n_ctr,
-                           near_ptr, near_idx, tgt_xyz, tgt_nrm, tgt_ptr, n_tgt, nullptr, 0,
+                           near_ptr, near_idx, nullptr, nullptr, tgt_xyz, tgt_nrm, tgt_ptr,
+                           n_tgt, nullptr, 0,
                            flags, 0, static_cast<char*>(workspace) + pbytes, ws_bytes - pbytes,
                            out, err_key, stream);
 }

@@ -349,6 +349,29 @@ __global__ void order_copy(const int32_t* __restrict__ order, const double* __re
   }
 }
 
+// one warp per 32-row slice: width = longest row; writes 32 * width (slice entries)
+__global__ void sell_width(const int64_t* __restrict__ nptr, int64_t n_rows,
+                           int64_t* __restrict__ wid) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (n_rows + 31) / 32 * 32) return;       // whole warps only
+  int64_t m = r < n_rows ? nptr[r + 1] - nptr[r] : 0;
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) wid[r >> 5] = 32 * ((m + 3) & ~3ll);   // width: multiple of 4
+}
+
+__global__ void sell_tail(int64_t* wid, int64_t n_sl) { wid[n_sl] = 0; }
+
+__global__ void sell_fill_kernel(const int64_t* __restrict__ nptr,
+                                 const int32_t* __restrict__ nidx, int64_t n_rows,
+                                 const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const int64_t b = nptr[r], len = nptr[r + 1] - b;
+  // blocks of 4 columns: entry (r, i) at sptr[slice] + (i / 4) * 128 + (r % 32) * 4 + i % 4
+  int32_t* base = sidx + sptr[r >> 5] + 4 * (r & 31);
+  for (int64_t i = 0; i < len; ++i) base[(i >> 2) * 128 + (i & 3)] = nidx[b + i];
+}
+
 __global__ void scatter_c128(int64_t n, const int64_t* __restrict__ dest,
                              const double2* __restrict__ src, double2* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -482,6 +505,46 @@ int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* c
                                                             tgt_nrm, n_ctr, tptr_out, ctr_out,
                                                             tgt_out, tnrm_out, tgt_index);
   return check_cuda(cudaGetLastError(), "order_targets launch");
+}
+
+int64_t tsqbx_sell_workspace_bytes(int64_t n_rows) {
+  if (n_rows < 0) return -1;
+  const int64_t n_sl = (n_rows + 31) / 32;
+  size_t t = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)(n_sl + 1));
+  return (int64_t)(align256((n_sl + 1) * sizeof(int64_t)) + align256(t));
+}
+
+int tsqbx_sell_size(int64_t n_rows, const int64_t* near_ptr, void* workspace, int64_t ws_bytes,
+                    int64_t* sell_ptr, int64_t* n_entries, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_rows < 0 || !workspace || ws_bytes < tsqbx_sell_workspace_bytes(n_rows) || !sell_ptr ||
+      !n_entries || (n_rows > 0 && !near_ptr))
+    return set_error(TSQBX_ERR_ARGUMENT, "sell_size: bad arguments");
+  const int64_t n_sl = (n_rows + 31) / 32;
+  char* ws = static_cast<char*>(workspace);
+  int64_t* wid = reinterpret_cast<int64_t*>(ws);
+  void* tmp = ws + align256((n_sl + 1) * sizeof(int64_t));
+  size_t tb = (size_t)ws_bytes - align256((n_sl + 1) * sizeof(int64_t));
+  if (n_sl > 0)
+    sell_width<<<(int)((n_sl * 32 + 255) / 256), 256, 0, st>>>(near_ptr, n_rows, wid);
+  sell_tail<<<1, 1, 0, st>>>(wid, n_sl);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, wid, sell_ptr, (int)(n_sl + 1), st);
+  cudaError_t e = cudaMemcpyAsync(n_entries, sell_ptr + n_sl, sizeof(int64_t),
+                                  cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "sell_size copy");
+  return check_cuda(cudaGetLastError(), "sell_size launch");
+}
+
+int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near_idx,
+                    const int64_t* sell_ptr, int32_t* sell_idx, void* stream) {
+  if (n_rows < 0 || (n_rows > 0 && (!near_ptr || !sell_ptr || !sell_idx)))
+    return set_error(TSQBX_ERR_ARGUMENT, "sell_fill: bad arguments");
+  if (n_rows == 0) return TSQBX_OK;
+  sell_fill_kernel<<<(int)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      near_ptr, near_idx, n_rows, sell_ptr, sell_idx);
+  return check_cuda(cudaGetLastError(), "sell_fill launch");
 }
 
 int tsqbx_scatter_c128(int64_t n, const int64_t* dest, const double* src, double* out,

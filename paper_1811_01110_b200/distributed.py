@@ -21,16 +21,18 @@ import torch
 import torch.distributed as dist
 
 
-def balanced_rows(row_pairs: np.ndarray, world: int) -> np.ndarray:
+def balanced_rows(row_pairs: np.ndarray, world: int, align: int = 32) -> np.ndarray:
     """Row boundaries b[0..world] splitting rows into `world` contiguous ranges of
-    (nearly) equal total pairs.  row_pairs[g] = len(row g) * targets(row g)."""
+    (nearly) equal total pairs.  row_pairs[g] = len(row g) * targets(row g).
+    Inner boundaries are multiples of `align` (SELL slices are 32 rows)."""
     row_pairs = np.asarray(row_pairs, dtype=np.int64)
     n = row_pairs.shape[0]
     cum = np.concatenate([[0], np.cumsum(row_pairs)])
     total = cum[-1]
     bounds = np.zeros(world + 1, dtype=np.int64)
     for r in range(1, world):
-        bounds[r] = int(np.searchsorted(cum, total * r / world, side="left"))
+        b = int(np.searchsorted(cum, total * r / world, side="left"))
+        bounds[r] = min(n, int(round(b / align)) * align)
     bounds[world] = n
     return np.maximum.accumulate(bounds)
 

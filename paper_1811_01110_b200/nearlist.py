@@ -44,10 +44,40 @@ class NearLists:
     idx: torch.Tensor
     src_perm: torch.Tensor | None = None
     ctr_order: torch.Tensor | None = None
+    sell_ptr: torch.Tensor | None = None
+    sell_idx: torch.Tensor | None = None
 
     @property
     def mean_len(self) -> float:
         return self.n_pairs / max(1, self.n_ctr)
+
+    def build_sell(self) -> "NearLists":
+        """Add the sliced-ELL (SELL-32) copy the thread-per-center kernels read:
+        slices of 32 rows, entries column-major (coalesced index loads)."""
+        if self.sell_ptr is not None:
+            return self
+        L = _lib.load()
+        dev = self.ptr.device
+        st = dv.stream_handle(dev)
+        n_sl = (self.n_ctr + 31) // 32
+        wsb = int(L.tsqbx_sell_workspace_bytes(self.n_ctr))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        sptr = torch.empty(n_sl + 1, dtype=torch.int64, device=dev)
+        n_ent = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.check(L.tsqbx_sell_size(self.n_ctr, self.ptr.data_ptr(), ws.data_ptr(), wsb,
+                                     sptr.data_ptr(), n_ent.data_ptr(), st), "tsqbx_sell_size")
+        sidx = torch.empty(max(int(n_ent.item()), 1), dtype=torch.int32, device=dev)
+        _lib.check(L.tsqbx_sell_fill(self.n_ctr, self.ptr.data_ptr(), self.idx.data_ptr(),
+                                     sptr.data_ptr(), sidx.data_ptr(), st), "tsqbx_sell_fill")
+        self.sell_ptr, self.sell_idx = sptr, sidx
+        return self
+
+    @property
+    def sell_fill(self) -> float:
+        """Fraction of SELL slots holding a real entry (1 - padding)."""
+        if self.sell_idx is None:
+            return float("nan")
+        return self.n_pairs / max(1, int(self.sell_ptr[-1].item()))
 
     @classmethod
     def from_user_csr(cls, ptr, idx, n_src: int, device=None) -> "NearLists":

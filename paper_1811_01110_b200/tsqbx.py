@@ -49,12 +49,20 @@ class TsConfig:
 
 
 def pick_group_lanes(mean_len: float) -> int:
-    """Lanes that share one center: ~4 list entries per lane, power of two in [1, 32]."""
+    """Lanes that share one center in the CSR (group) kernels: ~64 list entries
+    per lane, power of two in [1, 32].  Measured on B200 (profiles/): fewer
+    lanes amortise the per-center prologue and reduction better."""
     env = os.environ.get("GIGAQBX_GROUP_LANES")
     if env:
         return int(env)
-    g = 1 << max(0, int(round(math.log2(max(1.0, mean_len / 4.0)))))
+    g = 1 << max(0, int(round(math.log2(max(1.0, mean_len / 64.0)))))
     return max(1, min(32, g))
+
+
+def pick_layout() -> str:
+    """'sell' (thread per center on the sliced-ELL copy, the default) or 'csr'
+    (groups of lanes per center on the CSR rows); GIGAQBX_LAYOUT overrides."""
+    return os.environ.get("GIGAQBX_LAYOUT", "sell")
 
 
 def _equation_code(spec: KernelSpec) -> int:
@@ -117,6 +125,12 @@ class _Prepared:
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
         self.err = torch.empty(1, dtype=torch.int64, device=dev)
         self.G = int(group_lanes) if group_lanes else pick_group_lanes(near.mean_len)
+        self.layout = "csr" if group_lanes else pick_layout()
+        if self.layout == "sell" and self.n_ctr:
+            near.build_sell()
+        # Laplace densities are usually real: the kernel then skips Im w entirely
+        self.real_w = bool(self.eq == _lib.EQ_LAPLACE and self.n_src and
+                           not bool((w[:, 1] != 0).any().item()))
 
     def launch(self, out: torch.Tensor, validate: bool, generic: bool = False,
                rows: tuple[int, int] | None = None, out_offset: int = 0,
@@ -124,13 +138,19 @@ class _Prepared:
         """One evaluation launch.  ``rows=(g0, g1)`` restricts it to a row range
         (multi-GPU shard); ``user_order=False`` writes processing order."""
         L = _lib.load()
-        flags = (_lib.FLAG_VALIDATE if validate else 0) | (_lib.FLAG_GENERIC if generic else 0)
+        flags = ((_lib.FLAG_VALIDATE if validate else 0) | (_lib.FLAG_GENERIC if generic else 0)
+                 | (_lib.FLAG_REAL_WEIGHTS if self.real_w else 0))
         near = self.near
         g0, g1 = rows if rows is not None else (0, self.n_ctr)
+        sell = self.layout == "sell" and near.sell_ptr is not None
+        if sell and g0 % 32:
+            raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
         _lib.check(L.tsqbx_eval_packed(
             self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,
             self.with_normals, self.ctr.data_ptr() + 24 * g0, g1 - g0,
-            near.ptr.data_ptr() + 8 * g0, near.idx.data_ptr(), self.tgt.data_ptr(),
+            near.ptr.data_ptr() + 8 * g0, near.idx.data_ptr(),
+            near.sell_ptr.data_ptr() + 8 * (g0 // 32) if sell else None,
+            near.sell_idx.data_ptr() if sell else None, self.tgt.data_ptr(),
             dv.ptr(self.tn), self.tptr.data_ptr() + 8 * g0, self.n_tgt,
             dv.ptr(self.tidx) if user_order else None, out_offset, flags, self.G,
             self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.err.data_ptr(),
@@ -282,6 +302,10 @@ class TsqbxProblem:
     @property
     def group_lanes(self) -> int:
         return self.prep.G
+
+    @property
+    def layout(self) -> str:
+        return self.prep.layout
 
     def evaluate(self, validate: bool = False, generic: bool = False) -> torch.Tensor:
         if self.prep.n_tgt:

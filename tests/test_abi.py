@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_queries_without_gpu():
     L = _lib.load()
-    assert L.tsqbx_abi_version() == 1
+    assert L.tsqbx_abi_version() == 2
     assert L.tsqbx_packed_doubles(10, 0) == 52 and L.tsqbx_packed_doubles(10, 1) == 92
     assert L.tsqbx_eval_workspace_bytes(_lib.EQ_LAPLACE, 0, 8, 100) == 0
     assert L.tsqbx_eval_workspace_bytes(_lib.EQ_HELMHOLTZ, 0, 8, 100) >= 100 * 9 * 8
@@ -43,16 +43,16 @@ def test_abi_queries_without_gpu():
 def test_abi_rejects_bad_arguments_without_launching():
     L = _lib.load()
     rc = L.tsqbx_eval_packed(7, 0, 0.0, 4, None, 0, 0, None, 0, None, None, None, None, None,
-                             0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT and "equation" in _lib.last_error()
     rc = L.tsqbx_eval_packed(1, 0, -1.0, 4, None, 0, 0, None, 0, None, None, None, None, None,
-                             0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT and "k > 0" in _lib.last_error()
     rc = L.tsqbx_eval_packed(0, 0, 0.0, 65, None, 0, 0, None, 0, None, None, None, None, None,
-                             0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT
     rc = L.tsqbx_eval_packed(0, 2, 0.0, 4, None, 0, 0, None, 0, None, None, None, None, None,
-                             0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT and "normals" in _lib.last_error()
 
 
@@ -77,9 +77,9 @@ def test_config_validation_mirrors_reference():
 
 def test_group_lanes_heuristic(monkeypatch):
     monkeypatch.delenv("GIGAQBX_GROUP_LANES", raising=False)
-    assert tsqbx.pick_group_lanes(200) == 32
-    assert tsqbx.pick_group_lanes(12) == 4
-    assert tsqbx.pick_group_lanes(1) == 1
+    assert tsqbx.pick_group_lanes(200) == 4
+    assert tsqbx.pick_group_lanes(12) == 1
+    assert tsqbx.pick_group_lanes(4096) == 32
     monkeypatch.setenv("GIGAQBX_GROUP_LANES", "16")
     assert tsqbx.pick_group_lanes(200) == 16
 

@@ -1,0 +1,46 @@
+"""Time the evaluation of BASELINE cases over group sizes (device-resident, events).
+
+    python tools/sweep.py --cases c2/dense,c2/literal --lanes 4,8,16,32
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cases", default="c2/dense,c2/literal,c3/dense,c3/literal")
+ap.add_argument("--lanes", default="0")
+ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--peak", type=float, default=35.77)
+a = ap.parse_args()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for cs in a.cases.split(","):
+    name, preset = cs.split("/")
+    case = configs.make_case(name, preset)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    fpp = configs.algorithmic_flops_per_pair(case.cfg.spec, case.cfg.p_qbx)
+    for G in [int(x) for x in a.lanes.split(",")]:
+        prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                            near, tgt_ptr=case.tgt_ptr, group_lanes=G or None)
+        pairs = prob.pair_count()
+        for _ in range(3):
+            prob.evaluate()
+        ts = []
+        for _ in range(a.reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            prob.evaluate()
+            e1.record()
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = sorted(x.elapsed_time(y) for x, y in ts)[len(ts) // 2]
+        tf = pairs * fpp / (ms * 1e-3) / 1e12
+        print(f"{cs:12s} G={prob.group_lanes:2d} {ms:8.4f} ms  {pairs / ms / 1e6:8.2f} Gpairs/s "
+              f"{tf:6.2f} TF  {100 * tf / a.peak:5.1f}% of fp64 peak", flush=True)
+        del prob
