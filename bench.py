@@ -37,6 +37,17 @@ UNIT = "pair-evals/s"
 L2_FLUSH_BYTES = 256 << 20
 
 
+def _hbm_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0     # B200_PROFILING.md fallback
+
+
+HBM_PEAK = _hbm_peak()
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -333,7 +344,12 @@ def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
     fpp = configs.algorithmic_flops_per_pair(spec, case.cfg.p_qbx)
     mean_ms = sum(ms) / len(ms)
     launches_per_step = 1 if spec.is_laplace else 2
-    res = {"pairs_per_step": pairs, "ms": ms, "mean_ms": mean_ms,
+    # SURVEY.md 8(d) compulsory bytes: sources 40 B, centers 32 B, 4 B per CSR entry,
+    # targets 48 B (coordinates, output slot, potential)
+    alg_bytes = (case.n_sources * 40 + case.n_centers * 32 + near.n_pairs * 4
+                 + case.n_targets * 48)
+    res = {"pairs_per_step": pairs, "ms": ms, "mean_ms": mean_ms, "alg_bytes": alg_bytes,
+           "layout": prob.layout,
            "value": pairs * len(ms) / (sum(ms) * 1e-3), "flops_per_pair": fpp,
            "tflops": pairs * fpp / (mean_ms * 1e-3) / 1e12, "csr_build_ms": csr_ms,
            "group_lanes": prob.group_lanes, "launches_per_step": launches_per_step,
@@ -391,7 +407,8 @@ def main_ours(args):
                                      index=local)
     frac = res["tflops"] / peak if peak else None
     key = f"{case.name}/{case.preset}"
-    traffic = load_traffic(key)
+    tr = load_traffic(key)
+    traffic = tr["dram_bytes_per_launch"] if tr else None
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["mean_ms"],
@@ -401,7 +418,7 @@ def main_ours(args):
         "config": {"workload": workload_name(case), "case": case.name, "preset": case.preset,
                    "pairs_per_step": res["pairs_per_step"],
                    "mean_near_list": round(res["mean_list_len"], 2),
-                   "targets": case.n_targets, "group_lanes": res["group_lanes"],
+                   "targets": case.n_targets, "layout": res["layout"],
                    "l2": "flushed between steps (256 MB write, outside the timed events)",
                    "csr_build_ms": round(res["csr_build_ms"], 3), "seed": case.seed,
                    "validation": "off in `value` (driver path), on in `e2e` (public API)"},
@@ -411,6 +428,10 @@ def main_ours(args):
                      "peak_source": "measured DFMA probe on this GPU (tsqbx_fp64_probe); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                      "flops_per_pair": res["flops_per_pair"],
+                     "hbm": {"algorithmic_bytes": res["alg_bytes"],
+                             "achieved_gbs": res["alg_bytes"] / (res["mean_ms"] * 1e-3) / 1e9,
+                             "peak_gbs": HBM_PEAK,
+                             "note": "HBM is not the bound: flop/byte ~30 >> ridge ~5.5"},
                      "flops_convention": "algorithmic, SURVEY.md 8(d): Laplace 7p+17, "
                                          "Helmholtz 14p+30 per pair"},
         "gpu_launches": res["launches_per_step"] * args.steps,
@@ -442,7 +463,7 @@ def main_ours(args):
                 "value": r["value"], "pairs_per_step": r["pairs_per_step"],
                 "ms_per_step": r["mean_ms"], "tflops": r["tflops"],
                 "roofline_frac": r["tflops"] / peak if peak else None,
-                "group_lanes": r["group_lanes"], "csr_build_ms": round(r["csr_build_ms"], 3),
+                "layout": r["layout"], "csr_build_ms": round(r["csr_build_ms"], 3),
                 "mean_near_list": round(r["mean_list_len"], 2)}
             del p2
             torch.cuda.empty_cache()

@@ -14,7 +14,8 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libgigaqbx_tsqbx.so")
+LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
+                                                               "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
 # status codes (include/tsqbx.h)

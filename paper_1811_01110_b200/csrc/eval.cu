@@ -322,6 +322,16 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
 // DRAM latency of the CSR stream never reaches the arithmetic.  The source
 // record (an L1/L2 gather) is fetched one entry ahead into registers.
 constexpr int kSellBlock = 128;   // threads per CTA of the SELL kernels
+// minimum resident CTAs per SM requested from ptxas (caps registers per thread)
+#ifndef TSQBX_LAP_MINB
+#define TSQBX_LAP_MINB 6
+#endif
+#ifndef TSQBX_HELM_MINB
+#define TSQBX_HELM_MINB 4
+#endif
+#ifndef TSQBX_HELM_CF_SMEM
+#define TSQBX_HELM_CF_SMEM 0
+#endif
 constexpr int kRing = 4;          // index blocks in flight (16 entries of lookahead)
 
 struct SellStream {
@@ -376,7 +386,7 @@ struct SellStream {
 };
 
 template <int P, int NT, bool VAL, bool REALW>
-__global__ void __launch_bounds__(kSellBlock) laplace_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[(kRing + 1) * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.n_ctr) return;
@@ -385,9 +395,11 @@ __global__ void __launch_bounds__(kSellBlock) laplace_sell_kernel(const EvalPara
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+    int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       const bool ok = tb + q < t1;
+      slot[q] = ok ? out_slot(a, tb + q) : 0;
       tx[q] = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
       ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
       tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(kSellBlock) laplace_sell_kernel(const EvalPara
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
-        a.out[out_slot(a, tb + q)] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
+        a.out[slot[q]] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
         if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
           flag_suspect(a.err);
       }
@@ -427,10 +439,16 @@ __global__ void __launch_bounds__(kSellBlock) laplace_sell_kernel(const EvalPara
 }
 
 template <int P, int NT, bool VAL>
-__global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
   // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n live in shared
   // memory ([n][q][thread], conflict-free) instead of 2(P+1) registers per target
+#if TSQBX_HELM_CF_SMEM
   __shared__ double cfs[(P + 1) * NT * kSellBlock];
+#define CF(n, q) cfs[((n) * NT + (q)) * kSellBlock + tid]
+#else
+  double cfr[NT][P + 1];
+#define CF(n, q) cfr[q][n]
+#endif
   __shared__ int4 ring[(kRing + 1) * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.n_ctr) return;
@@ -441,9 +459,11 @@ __global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalPa
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+    int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       const bool ok = tb + q < t1;
+      slot[q] = ok ? out_slot(a, tb + q) : 0;
       const double ux = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
       const double uy = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
       const double uz = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
@@ -454,7 +474,7 @@ __global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalPa
       tz[q] = uz * ir;
 #pragma unroll
       for (int n = 0; n <= P; ++n)
-        cfs[(n * NT + q) * kSellBlock + tid] = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
+        CF(n, q) = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
       ar[q] = ai[q] = bm[q] = 0.0;
     }
     SellStream ss(a, g, len, false, ring);
@@ -472,11 +492,11 @@ __global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalPa
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         cg[q] = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
-        const double c0 = cfs[q * kSellBlock + tid];
+        const double c0 = CF(0, q);
         sr[q] = c0 * hmr;
         si[q] = c0 * hmi;
         if constexpr (P >= 1) {
-          const double c1 = cfs[(NT + q) * kSellBlock + tid] * cg[q];
+          const double c1 = CF(1, q) * cg[q];
           sr[q] = fma(c1, hcr, sr[q]);
           si[q] = fma(c1, hci, si[q]);
         }
@@ -497,7 +517,7 @@ __global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalPa
           const double pn = fma(c_leg.alpha[n] * cg[q], pc[q], -pm[q]);
           pm[q] = pc[q];
           pc[q] = pn;
-          const double c = cfs[((n + 1) * NT + q) * kSellBlock + tid] * pn;
+          const double c = CF(n + 1, q) * pn;
           sr[q] = fma(c, hnr, sr[q]);
           si[q] = fma(c, hni, si[q]);
         }
@@ -513,13 +533,14 @@ __global__ void __launch_bounds__(kSellBlock) helmholtz_sell_kernel(const EvalPa
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
-        a.out[out_slot(a, tb + q)] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
+        a.out[slot[q]] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
         if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
           flag_suspect(a.err);
       }
     }
   }
 }
+#undef CF
 
 // ---------------------------------------------------------------------------
 // Generic kernel: runtime order, every variant, reference operation order
