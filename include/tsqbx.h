@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 2
+#define TSQBX_ABI_VERSION 3
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -71,7 +71,9 @@ int tsqbx_device_info(int* sm_count, int* cc_major, int* cc_minor);
 /* ---------------------------------------------------------------------------
  * Source packing.  The evaluator reads sources in a packed, 32-byte aligned
  * layout: double4 {x, y, z, Re w} per source, then Im w per source, then (with
- * normals) double4 {nx, ny, nz, 0}.  packed[i] = source perm[i] (perm may be NULL).
+ * normals) double4 {nx, ny, nz, 0}, then 4 doubles of metadata (a device flag:
+ * some Im w != 0, which lets the Laplace kernels skip the imaginary part).
+ * packed[i] = source perm[i] (perm may be NULL).
  * ------------------------------------------------------------------------- */
 int64_t tsqbx_packed_doubles(int64_t n_src, int with_normals);
 int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const double* nrm,
@@ -149,21 +151,25 @@ int tsqbx_validate(const double* packed, int64_t n_src,
  *   tsqbx_near_count: Morton-sorts sources and centers, counts, scans.
  *       Writes src_perm (sorted position -> user source), ctr_order
  *       (processing position -> user center), near_ptr (n_ctr + 1, rows in
- *       processing order) and *n_pairs (device int64).
+ *       processing order), optionally sell_ptr (SELL-32x4 slice offsets,
+ *       ceil(n_ctr/32) + 1 entries) and totals[0] = n_pairs, totals[1] =
+ *       SELL entries (device int64[2]; one read-back sizes both index arrays).
  *   tsqbx_near_fill : writes near_idx (n_pairs entries, indices into the
- *       sorted source order, ascending within each row).
+ *       sorted source order, ascending within each row) and, when sell_idx is
+ *       given, the same lists in the SELL-32x4 layout.
  * ------------------------------------------------------------------------- */
 int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src);
 int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                      const double* src_xyz, int64_t n_src,
                      void* workspace, int64_t ws_bytes,
                      int32_t* src_perm, int32_t* ctr_order, int64_t* near_ptr,
-                     int64_t* n_pairs, void* stream);
+                     int64_t* sell_ptr, int64_t* totals, void* stream);
 int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                     const double* src_xyz, int64_t n_src,
                     void* workspace, int64_t ws_bytes,
                     const int32_t* ctr_order, const int64_t* near_ptr,
-                    int32_t* near_idx, void* stream);
+                    int32_t* near_idx, const int64_t* sell_ptr, int32_t* sell_idx,
+                    void* stream);
 
 /* Reorder centers and their targets into the processing order `ctr_order`
  * (user center ctr_order[g] becomes row g): writes ctr_out (n_ctr x 3),

@@ -24,7 +24,9 @@ def stream_handle(dev: torch.device) -> int:
 def to_device(a, dtype: torch.dtype, dev: torch.device, shape=None) -> torch.Tensor:
     """Contiguous device tensor of `dtype` (copies host arrays; no-op for matching tensors)."""
     if isinstance(a, torch.Tensor):
-        t = a.to(device=dev, dtype=dtype)
+        # pinned host tensors are copied asynchronously (stream-ordered DMA)
+        nb = bool(a.device.type == "cpu" and a.is_pinned() and a.dtype == dtype)
+        t = a.to(device=dev, dtype=dtype, non_blocking=nb)
     else:
         np_dtype = {torch.float64: np.float64, torch.int64: np.int64, torch.int32: np.int32,
                     torch.complex128: np.complex128}[dtype]

@@ -18,6 +18,8 @@ LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
                                                                "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
+ABI_VERSION = 3      # TSQBX_ABI_VERSION in include/tsqbx.h
+
 # status codes (include/tsqbx.h)
 OK = 0
 ERR_SEPARATION = 1
@@ -64,8 +66,8 @@ SIGNATURES = {
     "tsqbx_sell_size": (_I, [_I64, _P, _P, _I64, _P, _P, _P]),
     "tsqbx_sell_fill": (_I, [_I64, _P, _P, _P, _P, _P]),
     "tsqbx_near_workspace_bytes": (_I64, [_I64, _I64]),
-    "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
-    "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P]),
+    "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
+    "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_fp64_probe": (_I, [_P, _I64, _I, _I, _P]),
 }
 
@@ -99,8 +101,9 @@ def load():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.tsqbx_abi_version() != 2:
-            raise RuntimeError("TSQBX ABI version mismatch")
+        if L.tsqbx_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"TSQBX ABI version mismatch: library "
+                               f"{L.tsqbx_abi_version()}, bindings {ABI_VERSION}")
         _lib = L
     return _lib
 

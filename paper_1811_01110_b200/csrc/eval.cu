@@ -63,9 +63,13 @@ struct EvalParams {
   int G;
   int log2G;
   int validate;
-  int real_w;
+  int real_w;                        // host assertion: all Im w == 0
+  const unsigned* __restrict__ imag_flag;   // device: pack_kernel saw Im w != 0
   double k;
 };
+
+int64_t packed_doubles(int64_t n, int with_normals);
+int64_t packed_meta_offset(int64_t n, int with_normals);
 
 __device__ __forceinline__ int64_t out_slot(const EvalParams& a, int64_t t) {
   return (a.tout ? a.tout[t] : t) - a.out_offset;
@@ -386,10 +390,7 @@ struct SellStream {
 };
 
 template <int P, int NT, bool VAL, bool REALW>
-__global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
-  __shared__ int4 ring[(kRing + 1) * kSellBlock];
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.n_ctr) return;
+__device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g, int4* ring) {
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
@@ -436,6 +437,19 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kerne
       }
     }
   }
+}
+
+// real weights (the usual Laplace density) skip every Im w load and FMA; the
+// pack kernel records whether any Im w is nonzero, so no host round trip decides
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
+  __shared__ int4 ring[(kRing + 1) * kSellBlock];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.n_ctr) return;
+  if (a.real_w || *a.imag_flag == 0u)
+    laplace_sell_body<P, NT, VAL, true>(a, g, ring);
+  else
+    laplace_sell_body<P, NT, VAL, false>(a, g, ring);
 }
 
 template <int P, int NT, bool VAL>
@@ -820,13 +834,19 @@ __global__ void validate_kernel(const double4* __restrict__ sp, const double* __
 __global__ void pack_kernel(int64_t n, const double* __restrict__ xyz,
                             const double* __restrict__ w, const double* __restrict__ nrm,
                             const int32_t* __restrict__ perm, double4* __restrict__ sp,
-                            double* __restrict__ swi, double4* __restrict__ snrm) {
+                            double* __restrict__ swi, double4* __restrict__ snrm,
+                            unsigned* __restrict__ imag_flag) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t s = perm ? (int64_t)perm[i] : i;
-  sp[i] = make_double4(xyz[3 * s], xyz[3 * s + 1], xyz[3 * s + 2], w[2 * s]);
-  swi[i] = w[2 * s + 1];
-  if (nrm) snrm[i] = make_double4(nrm[3 * s], nrm[3 * s + 1], nrm[3 * s + 2], 0.0);
+  bool imag = false;
+  if (i < n) {
+    const int64_t s = perm ? (int64_t)perm[i] : i;
+    sp[i] = make_double4(xyz[3 * s], xyz[3 * s + 1], xyz[3 * s + 2], w[2 * s]);
+    const double wi = w[2 * s + 1];
+    swi[i] = wi;
+    imag = wi != 0.0;
+    if (nrm) snrm[i] = make_double4(nrm[3 * s], nrm[3 * s + 1], nrm[3 * s + 2], 0.0);
+  }
+  if (__any_sync(0xffffffffu, imag) && (threadIdx.x & 31) == 0) atomicOr(imag_flag, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -839,8 +859,7 @@ void launch_fast(int equation, bool sell, const EvalParams& a, int64_t n_ctr, cu
   if (sell) {
     const int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
     if (equation == TSQBX_EQ_LAPLACE) {
-      if (a.real_w) laplace_sell_kernel<P, NT, VAL, true><<<blocks, kSellBlock, 0, st>>>(a);
-      else laplace_sell_kernel<P, NT, VAL, false><<<blocks, kSellBlock, 0, st>>>(a);
+      laplace_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     } else {
       helmholtz_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     }
@@ -877,9 +896,14 @@ struct FastTable {
 };
 using FastOrders = FastTable<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
 
+// [x y z Re w]*n | Im w * n | pad to 4 | [nx ny nz 0]*n (optional) | meta (4 doubles)
+// meta[0] (as uint32) = 1 if any Im w != 0 (written by pack_kernel)
 int64_t packed_doubles(int64_t n, int with_normals) {
   const int64_t base = (5 * n + 3) / 4 * 4;  // keep the normals 32-byte aligned
-  return with_normals ? base + 4 * n : base;
+  return (with_normals ? base + 4 * n : base) + 4;
+}
+int64_t packed_meta_offset(int64_t n, int with_normals) {
+  return packed_doubles(n, with_normals) - 4;
 }
 
 }  // namespace tsqbx
@@ -909,15 +933,23 @@ int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const 
                        const int32_t* perm, double* packed, void* stream) {
   if (n_src < 0 || (n_src > 0 && (!xyz || !w || !packed)))
     return set_error(TSQBX_ERR_ARGUMENT, "pack_sources: bad arguments");
-  if (n_src == 0) return TSQBX_OK;
-  if (((uintptr_t)packed) & 31)
+  if (n_src > 0 && (((uintptr_t)packed) & 31))
     return set_error(TSQBX_ERR_ARGUMENT, "pack_sources: packed buffer must be 32-byte aligned");
-  const int64_t base = packed_doubles(n_src, 0);
+  if (n_src == 0) {
+    if (packed) return check_cuda(cudaMemsetAsync(packed, 0, 4 * sizeof(double),
+                                                  (cudaStream_t)stream), "pack memset");
+    return TSQBX_OK;
+  }
+  const int64_t base = (5 * n_src + 3) / 4 * 4;
   double4* sp = reinterpret_cast<double4*>(packed);
   double* swi = packed + 4 * n_src;
   double4* sn = nrm ? reinterpret_cast<double4*>(packed + base) : nullptr;
+  unsigned* flag = reinterpret_cast<unsigned*>(packed + packed_meta_offset(n_src, nrm != nullptr));
+  cudaError_t e = cudaMemsetAsync(flag, 0, 4 * sizeof(double), (cudaStream_t)stream);
+  if (e != cudaSuccess) return check_cuda(e, "pack_sources memset");
   const int blocks = (int)((n_src + 255) / 256);
-  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_src, xyz, w, nrm, perm, sp, swi, sn);
+  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_src, xyz, w, nrm, perm, sp, swi, sn,
+                                                          flag);
   return check_cuda(cudaGetLastError(), "pack_kernel launch");
 }
 
@@ -965,8 +997,9 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   EvalParams a{};
   a.sp = reinterpret_cast<const double4*>(packed);
   a.swi = packed + 4 * n_src;
-  a.snrm = with_normals ? reinterpret_cast<const double4*>(packed + packed_doubles(n_src, 0))
+  a.snrm = with_normals ? reinterpret_cast<const double4*>(packed + (5 * n_src + 3) / 4 * 4)
                         : nullptr;
+  a.imag_flag = reinterpret_cast<const unsigned*>(packed + packed_meta_offset(n_src, with_normals));
   a.ctr = ctr_xyz;
   a.nptr = near_ptr;
   a.nidx = near_idx;

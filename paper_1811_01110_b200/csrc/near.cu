@@ -28,7 +28,7 @@ constexpr int kSubBits = 3;  // coarse cell = 8 fine cells per axis
 
 struct NearLayout {
   size_t off_mm, off_prm, off_skey_in, off_skey, off_sval_in, off_ckey_in, off_ckey, off_cval_in,
-      off_sxyz, off_hkey, off_hst, off_hen, off_cnt, off_tmp, total;
+      off_sxyz, off_hkey, off_hst, off_hen, off_cnt, off_wid, off_tmp, total;
   int64_t cap;
   size_t tmp_bytes;
 };
@@ -59,7 +59,9 @@ NearLayout near_layout(int64_t n_ctr, int64_t n_src) {
   L.off_hst = take(cap * sizeof(int32_t));
   L.off_hen = take(cap * sizeof(int32_t));
   L.off_cnt = take((n_ctr + 1) * sizeof(int64_t));
-  size_t t1 = 0, t2 = 0, t3 = 0;
+  const int64_t n_sl = (n_ctr + 31) / 32;
+  L.off_wid = take((n_sl + 1) * sizeof(int64_t));
+  size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t1, (unsigned long long*)nullptr,
                                   (unsigned long long*)nullptr, (int32_t*)nullptr,
                                   (int32_t*)nullptr, (int)n_src, 0, 3 * kFineBits);
@@ -68,7 +70,9 @@ NearLayout near_layout(int64_t n_ctr, int64_t n_src) {
                                   (int32_t*)nullptr, (int)n_ctr, 0, 3 * kFineBits);
   cub::DeviceScan::ExclusiveSum(nullptr, t3, (int64_t*)nullptr, (int64_t*)nullptr,
                                 (int)(n_ctr + 1));
-  L.tmp_bytes = std::max(t1, std::max(t2, t3)) + 256;
+  cub::DeviceScan::ExclusiveSum(nullptr, t4, (int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)(n_sl + 1));
+  L.tmp_bytes = std::max(std::max(t1, t4), std::max(t2, t3)) + 256;
   L.off_tmp = take(L.tmp_bytes);
   L.total = o;
   return L;
@@ -254,7 +258,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(
     const int32_t* __restrict__ order, const double* __restrict__ prm,
     const double4* __restrict__ sxyz, const unsigned long long* __restrict__ hkey,
     const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
-    int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx) {
+    int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
+    const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= n_ctr) return;
@@ -294,7 +299,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(
     }
   }
   int64_t count = 0;
-  int64_t out = FILL ? nptr[g] : 0;
+  const int64_t row0 = FILL ? nptr[g] : 0;
+  int64_t out = row0;
+  // SELL-32x4 slot of row entry i: sptr[g/32] + (i/4)*128 + (g%32)*4 + i%4
+  int32_t* sbase = (FILL && sidx) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
   for (int L = 0; L < 27; ++L) {
     const unsigned long long k = __shfl_sync(0xffffffffu, key, L);
     if (k == kEmpty) break;
@@ -304,7 +312,14 @@ __global__ void __launch_bounds__(256) sweep_kernel(
       const int j = base + lane;
       const bool m = j < ce && member(sxyz[j], cx, cy, cz, rad2);
       const unsigned bal = __ballot_sync(0xffffffffu, m);
-      if (FILL && m) nidx[out + __popc(bal & ((1u << lane) - 1u))] = j;
+      if (FILL && m) {
+        const int64_t at = out + __popc(bal & ((1u << lane) - 1u));
+        nidx[at] = j;
+        if (sbase) {
+          const int64_t i = at - row0;
+          sbase[(i >> 2) * 128 + (i & 3)] = j;
+        }
+      }
       out += __popc(bal);
       count += __popc(bal);
     }
@@ -312,7 +327,71 @@ __global__ void __launch_bounds__(256) sweep_kernel(
   if (!FILL && lane == 0) cnt[g] = count;
 }
 
+// one THREAD per center (processing order): consecutive threads hold
+// Morton-adjacent centers, so their 27-cell neighbourhoods overlap and the
+// candidate loads hit L1.  Row order = cell enumeration (dz, dy, dx) order,
+// ascending within a cell.  FILL writes the CSR row and its SELL-32x4 column.
+template <bool FILL>
+__global__ void __launch_bounds__(128) sweep_thread_kernel(
+    const double* ctr, const double* rad, int64_t n_ctr,
+    const int32_t* order, const double* prm,
+    const double4* sxyz, const unsigned long long* hkey,
+    const int32_t* hst, const int32_t* hen, int64_t cap,
+    int64_t* cnt, const int64_t* nptr, int32_t* nidx,
+    const int64_t* sptr, int32_t* sidx) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_ctr) return;
+  const int64_t ic = order[g];
+  const double cx = ctr[3 * ic], cy = ctr[3 * ic + 1], cz = ctr[3 * ic + 2];
+  const double r = rad[ic];
+  const double rad2 = __dmul_rn(r, r);
+  const double pl[3] = {cx, cy, cz};
+  const double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
+  unsigned long long f[3];
+  fine_coords(pl, prm_l, f);
+  const unsigned long long ccx = f[0] >> kSubBits, ccy = f[1] >> kSubBits, ccz = f[2] >> kSubBits;
+  int32_t* row = FILL ? nidx + nptr[g] : nullptr;
+  int32_t* sbase = (FILL && sidx) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
+  int k = 0;
+  for (int dx = 0; dx < 3; ++dx) {
+   for (int dy = 0; dy < 3; ++dy) {
+    for (int dz = 0; dz < 3; ++dz) {
+    const unsigned long long key = morton3(ccx + dx - 1, ccy + dy - 1, ccz + dz - 1);
+    int st = 0, en = 0;
+    if (!hash_find(hkey, hst, hen, cap, key, st, en)) en = st;
+    for (int j = st; j < en; ++j) {
+      if (member(sxyz[j], cx, cy, cz, rad2)) {
+        if (FILL) {
+          row[k] = j;
+          if (sbase) sbase[(k >> 2) * 128 + (k & 3)] = j;
+        }
+        ++k;
+      }
+    }
+    }
+   }
+  }
+  if (!FILL) cnt[g] = k;
+#ifdef TSQBX_DEBUG_FILL
+  if (FILL && cnt && k != nptr[g + 1] - nptr[g]) atomicAdd((unsigned long long*)cnt, 1ull);
+#endif
+}
+
 __global__ void set_tail(int64_t* cnt, int64_t n) { cnt[n] = 0; }
+
+// one warp per 32-row slice: width = longest row; writes 32 * width (slice entries)
+__global__ void sell_width(const int64_t* __restrict__ nptr, int64_t n_rows,
+                           int64_t* __restrict__ wid) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (n_rows + 31) / 32 * 32) return;       // whole warps only
+  int64_t m = r < n_rows ? nptr[r + 1] - nptr[r] : 0;
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) wid[r >> 5] = 32 * ((m + 3) & ~3ll);   // width: multiple of 4
+}
+
+__global__ void sell_tail(int64_t* wid, int64_t n_sl) { wid[n_sl] = 0; }
+
+
 
 // --- targets into processing order -------------------------------------------
 __global__ void order_count(const int32_t* __restrict__ order, const int64_t* __restrict__ tptr,
@@ -349,18 +428,6 @@ __global__ void order_copy(const int32_t* __restrict__ order, const double* __re
   }
 }
 
-// one warp per 32-row slice: width = longest row; writes 32 * width (slice entries)
-__global__ void sell_width(const int64_t* __restrict__ nptr, int64_t n_rows,
-                           int64_t* __restrict__ wid) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= (n_rows + 31) / 32 * 32) return;       // whole warps only
-  int64_t m = r < n_rows ? nptr[r + 1] - nptr[r] : 0;
-  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if ((threadIdx.x & 31) == 0) wid[r >> 5] = 32 * ((m + 3) & ~3ll);   // width: multiple of 4
-}
-
-__global__ void sell_tail(int64_t* wid, int64_t n_sl) { wid[n_sl] = 0; }
-
 __global__ void sell_fill_kernel(const int64_t* __restrict__ nptr,
                                  const int32_t* __restrict__ nidx, int64_t n_rows,
                                  const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
@@ -392,8 +459,8 @@ int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src) {
 
 int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                      const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
-                     int32_t* src_perm, int32_t* ctr_order, int64_t* near_ptr, int64_t* n_pairs,
-                     void* stream) {
+                     int32_t* src_perm, int32_t* ctr_order, int64_t* near_ptr,
+                     int64_t* sell_ptr, int64_t* totals, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_ctr < 0 || n_src < 0 || n_src > INT32_MAX - 64 || n_ctr > INT32_MAX - 64)
     return set_error(TSQBX_ERR_ARGUMENT, "near_count: bad sizes");
@@ -401,7 +468,7 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
   if (!workspace || ws_bytes < (int64_t)L.total)
     return set_error(TSQBX_ERR_ARGUMENT, "near_count: workspace too small (need %lld)",
                      (long long)L.total);
-  if (!near_ptr || !n_pairs || (n_ctr > 0 && (!ctr_xyz || !radius || !ctr_order)) ||
+  if (!near_ptr || !totals || (n_ctr > 0 && (!ctr_xyz || !radius || !ctr_order)) ||
       (n_src > 0 && (!src_xyz || !src_perm)))
     return set_error(TSQBX_ERR_ARGUMENT, "near_count: null array");
   char* ws = static_cast<char*>(workspace);
@@ -420,6 +487,9 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
   auto* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
   void* tmp = ws + L.off_tmp;
 
+#ifdef TSQBX_DEBUG_FILL
+  cudaMemsetAsync(workspace, 0, L.total, st);
+#endif
   init_bounds<<<1, 32, 0, st>>>(mm);
   if (n_src + n_ctr > 0) {
     int nb = (int)std::min<int64_t>((n_src + n_ctr + 255) / 256, 148 * 8);
@@ -441,23 +511,35 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     tb = L.tmp_bytes;
     cub::DeviceRadixSort::SortPairs(tmp, tb, ckey_in, ckey, cval_in, ctr_order, (int)n_ctr, 0,
                                     3 * kFineBits, st);
-    sweep_kernel<false><<<(int)((n_ctr * 32 + 255) / 256), 256, 0, st>>>(
+    sweep_thread_kernel<false><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
         ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, cnt, nullptr,
-        nullptr);
+        nullptr, nullptr, nullptr);
   }
   set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
   tb = L.tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
-  cudaError_t e = cudaMemcpyAsync(n_pairs, near_ptr + n_ctr, sizeof(int64_t),
+  cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t),
                                   cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return check_cuda(e, "near_count copy");
+  if (sell_ptr) {                       // SELL-32x4 offsets from the row lengths
+    const int64_t n_sl = (n_ctr + 31) / 32;
+    int64_t* wid = reinterpret_cast<int64_t*>(ws + L.off_wid);
+    if (n_sl > 0)
+      sell_width<<<(int)((n_sl * 32 + 255) / 256), 256, 0, st>>>(near_ptr, n_ctr, wid);
+    sell_tail<<<1, 1, 0, st>>>(wid, n_sl);
+    tb = L.tmp_bytes;
+    cub::DeviceScan::ExclusiveSum(tmp, tb, wid, sell_ptr, (int)(n_sl + 1), st);
+    e = cudaMemcpyAsync(totals + 1, sell_ptr + n_sl, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                        st);
+    if (e != cudaSuccess) return check_cuda(e, "near_count copy");
+  }
   return check_cuda(cudaGetLastError(), "near_count launch");
 }
 
 int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                     const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
                     const int32_t* ctr_order, const int64_t* near_ptr, int32_t* near_idx,
-                    void* stream) {
+                    const int64_t* sell_ptr, int32_t* sell_idx, void* stream) {
   (void)src_xyz;
   cudaStream_t st = (cudaStream_t)stream;
   const NearLayout L = near_layout(n_ctr, n_src);
@@ -465,12 +547,18 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     return set_error(TSQBX_ERR_ARGUMENT, "near_fill: workspace too small");
   if (n_ctr == 0) return TSQBX_OK;
   char* ws = static_cast<char*>(workspace);
-  sweep_kernel<true><<<(int)((n_ctr * 32 + 255) / 256), 256, 0, st>>>(
+  sweep_thread_kernel<true><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
       ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
       reinterpret_cast<const double4*>(ws + L.off_sxyz),
       reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
       reinterpret_cast<const int32_t*>(ws + L.off_hst),
-      reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, nullptr, near_ptr, near_idx);
+      reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap,
+#ifdef TSQBX_DEBUG_FILL
+      reinterpret_cast<int64_t*>(ws + L.off_wid), near_ptr, near_idx,
+#else
+      nullptr, near_ptr, near_idx,
+#endif
+      sell_idx ? sell_ptr : nullptr, sell_idx);
   return check_cuda(cudaGetLastError(), "near_fill launch");
 }
 

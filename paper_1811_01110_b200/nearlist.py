@@ -108,12 +108,13 @@ class NearLists:
         return uptr, uidx.astype(np.int32)
 
 
-def build_near_lists(centers, sources, radii, device=None) -> NearLists:
+def build_near_lists(centers, sources, radii, device=None, sell: bool = True) -> NearLists:
     """Radius-ball near lists {s : |s - c|^2 <= rad_c^2} on the device.
 
     centers (n_ctr, 3), sources (n_src, 3), radii scalar or (n_ctr,) -- numpy
     arrays or torch tensors.  Returns a device :class:`NearLists` in Morton
-    processing order.
+    processing order, with the SELL-32x4 copy the fast kernels read (``sell``).
+    One host read-back (the two totals) sizes the index arrays.
     """
     dev = dv.require_cuda(device)
     L = _lib.load()
@@ -133,16 +134,19 @@ def build_near_lists(centers, sources, radii, device=None) -> NearLists:
     src_perm = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
     ctr_order = torch.empty(max(n_ctr, 1), dtype=torch.int32, device=dev)
     nptr = torch.empty(n_ctr + 1, dtype=torch.int64, device=dev)
-    npairs = torch.zeros(1, dtype=torch.int64, device=dev)
+    sptr = torch.empty((n_ctr + 31) // 32 + 1, dtype=torch.int64, device=dev) if sell else None
+    totals = torch.zeros(2, dtype=torch.int64, device=dev)
     _lib.check(L.tsqbx_near_count(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
                                   ws.data_ptr(), ws_bytes, src_perm.data_ptr(),
-                                  ctr_order.data_ptr(), nptr.data_ptr(), npairs.data_ptr(), st),
-               "tsqbx_near_count")
-    n_pairs = int(npairs.item())
+                                  ctr_order.data_ptr(), nptr.data_ptr(), dv.ptr(sptr),
+                                  totals.data_ptr(), st), "tsqbx_near_count")
+    n_pairs, n_sell = (int(v) for v in totals.cpu().tolist())
     idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
+    sidx = torch.empty(max(n_sell, 4), dtype=torch.int32, device=dev) if sell else None
     _lib.check(L.tsqbx_near_fill(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
                                  ws.data_ptr(), ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
-                                 idx.data_ptr(), st),
+                                 idx.data_ptr(), dv.ptr(sptr), dv.ptr(sidx), st),
                "tsqbx_near_fill")
     return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr, idx=idx[:n_pairs],
-                     src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr])
+                     src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],
+                     sell_ptr=sptr, sell_idx=sidx)

@@ -128,9 +128,9 @@ class _Prepared:
         self.layout = "csr" if group_lanes else pick_layout()
         if self.layout == "sell" and self.n_ctr:
             near.build_sell()
-        # Laplace densities are usually real: the kernel then skips Im w entirely
-        self.real_w = bool(self.eq == _lib.EQ_LAPLACE and self.n_src and
-                           not bool((w[:, 1] != 0).any().item()))
+        # real Laplace densities: the pack kernel flags any Im w != 0 on the device
+        # and the kernel picks its real-weight path itself (no host round trip)
+        self.real_w = False
 
     def launch(self, out: torch.Tensor, validate: bool, generic: bool = False,
                rows: tuple[int, int] | None = None, out_offset: int = 0,
@@ -212,7 +212,8 @@ def _inputs(cfg, sources, weights, centers, targets, source_normals, target_norm
 
 def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
                         tgt_ptr=None, source_normals=None, target_normals=None,
-                        validate: bool = True, group_lanes: int | None = None, device=None):
+                        validate: bool = True, group_lanes: int | None = None, device=None,
+                        out=None):
     """Per-target TSQBX potentials for many centers in one launch.
 
     sources (n_src, 3), weights (n_src,) complex, centers (n_ctr, 3),
@@ -241,22 +242,37 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
         nptr, nidx = near
         near = NearLists.from_user_csr(nptr, nidx, int(src.shape[0]), dev)
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
-    out = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
+    res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
-        prep.launch(torch.view_as_real(out), validate)
+        prep.launch(torch.view_as_real(res), validate)
         if validate:
             prep.check_errors(batch_context=True)
-    return out.cpu().numpy() if host_out else out
+    return _deliver(res, out, host_out)
+
+
+def _deliver(out_dev: torch.Tensor, out, host_out: bool):
+    """Result hand-off: into a caller buffer (a pinned host tensor makes the D2H a
+    direct DMA), else numpy for host inputs / the CUDA tensor for device inputs."""
+    if out is not None:
+        if isinstance(out, np.ndarray):
+            out[...] = out_dev.cpu().numpy()
+        else:
+            out.copy_(out_dev)
+        return out
+    return out_dev.cpu().numpy() if host_out else out_dev
 
 
 def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, targets,
                           tgt_ptr=None, source_normals=None, target_normals=None,
-                          validate: bool = True, group_lanes: int | None = None, device=None):
+                          validate: bool = True, group_lanes: int | None = None, device=None,
+                          out=None):
     """The whole near-field path in one call: geometry -> device radius-ball near
     lists (``build_near_lists``) -> TSQBX evaluation -> per-target potentials.
 
-    Host inputs are copied to the device once; the result comes back as numpy
-    (or stays a CUDA tensor when ``sources`` is one)."""
+    Host inputs are copied to the device once (asynchronously when they are
+    pinned tensors); the result comes back as numpy, into ``out`` (e.g. a
+    pinned complex128 tensor) when given, or stays a CUDA tensor when
+    ``sources`` is one."""
     from .nearlist import build_near_lists
 
     host_out = not (isinstance(sources, torch.Tensor) and sources.is_cuda)
@@ -271,12 +287,12 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
             else dv.to_device(tgt_ptr, torch.int64, dev))
     near = build_near_lists(ctr, src, rad, dev)
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
-    out = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
+    res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
-        prep.launch(torch.view_as_real(out), validate)
+        prep.launch(torch.view_as_real(res), validate)
         if validate:
             prep.check_errors(batch_context=True)
-    return out.cpu().numpy() if host_out else out
+    return _deliver(res, out, host_out)
 
 
 class TsqbxProblem:
