@@ -155,8 +155,9 @@ int tsqbx_validate(const double* packed, int64_t n_src,
  *       ceil(n_ctr/32) + 1 entries) and totals[0] = n_pairs, totals[1] =
  *       SELL entries (device int64[2]; one read-back sizes both index arrays).
  *   tsqbx_near_fill : writes near_idx (n_pairs entries, indices into the
- *       sorted source order, ascending within each row) and, when sell_idx is
- *       given, the same lists in the SELL-32x4 layout.
+ *       sorted source order; may be NULL) and, when sell_idx is given, the
+ *       same lists in the SELL-32x4 layout.  Row order: the 27 neighbour
+ *       cells in (dx, dy, dz) order, ascending within a cell.
  * ------------------------------------------------------------------------- */
 int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src);
 int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
@@ -195,6 +196,10 @@ int tsqbx_sell_size(int64_t n_rows, const int64_t* near_ptr, void* workspace, in
                     int64_t* sell_ptr, int64_t* n_entries, void* stream);
 int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near_idx,
                     const int64_t* sell_ptr, int32_t* sell_idx, void* stream);
+
+/* CSR entries (near_idx, rows by near_ptr) from a SELL-32x4 copy. */
+int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,
+                      const int32_t* sell_idx, int32_t* near_idx, void* stream);
 
 /* out[dest[i]] = src[i] for n complex128 values (dest NULL = copy); assembles
  * all-gathered shards into user target order. */

@@ -39,7 +39,7 @@ def _one(spec: KernelSpec, p, sources, weights, snormals, center, target, tnorma
                                         snormals, tn, dev)
     near = NearLists(n_ctr=1, n_src=n, n_pairs=n,
                      ptr=torch.tensor([0, n], dtype=torch.int64, device=dev),
-                     idx=torch.arange(n, dtype=torch.int32, device=dev))
+                     csr_idx=torch.arange(n, dtype=torch.int32, device=dev))
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tnd,
                      torch.tensor([0, 1], dtype=torch.int64, device=dev))
     out = torch.empty(1, dtype=torch.complex128, device=dev)

@@ -994,6 +994,8 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   if (n_ctr == 0 || n_tgt == 0) return check_cuda(cudaGetLastError(), "eval");
 
   const bool fast = variant == 0 && p <= kMaxFastOrder && !(flags & TSQBX_FLAG_GENERIC);
+  if (!(fast && sell_ptr) && !near_idx)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_idx (CSR entries) required for this kernel");
   EvalParams a{};
   a.sp = reinterpret_cast<const double4*>(packed);
   a.swi = packed + 4 * n_src;

@@ -142,13 +142,24 @@ __global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
     }
     rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, off));
   }
+  // block reduction through shared memory, then one atomic per value per block
+  __shared__ long long red[7][32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      atomicMin(&mm[d], lo[d]);
-      atomicMax(&mm[3 + d], hi[d]);
+      red[d][w] = lo[d];
+      red[3 + d][w] = hi[d];
     }
-    atomicMax(&mm[6], rm);
+    red[6][w] = rm;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int v = threadIdx.x;
+    long long acc = red[v][0];
+    for (int q = 1; q < nw; ++q) acc = v < 3 ? min(acc, red[v][q]) : max(acc, red[v][q]);
+    if (v < 3) atomicMin(&mm[v], acc);
+    else atomicMax(&mm[v], acc);
   }
 }
 
@@ -377,6 +388,147 @@ __global__ void __launch_bounds__(128) sweep_thread_kernel(
 #endif
 }
 
+// one WARP per 32 consecutive centers (processing order).  Consecutive centers
+// share their coarse cell (Morton order), so the warp walks the distinct cells
+// of its lanes; for each cell the 27 neighbour cells are looked up once (lane
+// l < 27 probes neighbour l) and their sources are staged into a per-warp
+// shared-memory tile of kTile candidates (all neighbour-cell copies issued
+// back to back, coalesced), which every lane of that cell then tests with
+// broadcast reads.  Row order = neighbour order (dx, dy, dz), ascending within
+// a cell -- identical in the count and the fill pass.
+constexpr int kTile = 256;
+
+template <bool FILL>
+__global__ void __launch_bounds__(128) sweep_cell_kernel(
+    const double* __restrict__ ctr, const double* __restrict__ rad, int64_t n_ctr,
+    const int32_t* __restrict__ order, const double* __restrict__ prm,
+    const double4* __restrict__ sxyz, const unsigned long long* __restrict__ hkey,
+    const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
+    int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
+    const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
+  __shared__ double4 tile[4][kTile];
+  __shared__ int32_t tid_[4][kTile];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = g < n_ctr;
+  double cx = 0.0, cy = 0.0, cz = 0.0, rad2 = -1.0;
+  unsigned long long ccx = 0, ccy = 0, ccz = 0, ckey = kEmpty;
+  if (valid) {
+    const int64_t ic = order[g];
+    cx = ctr[3 * ic];
+    cy = ctr[3 * ic + 1];
+    cz = ctr[3 * ic + 2];
+    const double r = rad[ic];
+    rad2 = __dmul_rn(r, r);
+    const double pl[3] = {cx, cy, cz};
+    const double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
+    unsigned long long f[3];
+    fine_coords(pl, prm_l, f);
+    ccx = f[0] >> kSubBits;
+    ccy = f[1] >> kSubBits;
+    ccz = f[2] >> kSubBits;
+    ckey = morton3(ccx, ccy, ccz);
+  }
+  int32_t* row = (FILL && valid && nidx) ? nidx + nptr[g] : nullptr;
+  // SELL-32x4 column of this row as int4 blocks: block b at sblk[32 b]
+  int4* sblk = (FILL && valid && sidx) ? reinterpret_cast<int4*>(sidx + sptr[g >> 5]) + (g & 31)
+                                       : nullptr;
+  int4 pend = make_int4(0, 0, 0, 0);   // entries of the current SELL block not yet stored
+  const unsigned long long prev = __shfl_up_sync(0xffffffffu, ckey, 1);
+  unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || prev != ckey));
+  int k = 0;
+  while (heads) {
+    const int a = __ffs(heads) - 1;
+    heads &= heads - 1;
+    const unsigned long long cell = __shfl_sync(0xffffffffu, ckey, a);
+    const unsigned long long bx = __shfl_sync(0xffffffffu, ccx, a);
+    const unsigned long long by = __shfl_sync(0xffffffffu, ccy, a);
+    const unsigned long long bz = __shfl_sync(0xffffffffu, ccz, a);
+    const bool mine = valid && ckey == cell;
+    int st = 0, en = 0;
+    if (lane < 27) {
+      const unsigned long long nk =
+          morton3(bx + (lane / 9) - 1, by + ((lane / 3) % 3) - 1, bz + (lane % 3) - 1);
+      if (!hash_find(hkey, hst, hen, cap, nk, st, en)) en = st;
+    }
+    // walk the neighbour cells in order, filling the tile; flush when full
+    int fill = 0;            // candidates staged in the tile
+    int nb = 0, pos = 0;     // next neighbour cell and position inside it
+    int cs = __shfl_sync(0xffffffffu, st, 0), ce = __shfl_sync(0xffffffffu, en, 0);
+    while (true) {
+      // stage candidates until the tile is full or every neighbour is done
+      while (nb < 27 && fill < kTile) {
+        const int take = min(ce - (cs + pos), kTile - fill);
+        for (int q = lane; q < take; q += 32) {
+          const int j = cs + pos + q;
+          tile[wib][fill + q] = sxyz[j];
+          tid_[wib][fill + q] = j;
+        }
+        fill += take;
+        pos += take;
+        if (cs + pos >= ce) {
+          ++nb;
+          pos = 0;
+          if (nb < 27) {
+            cs = __shfl_sync(0xffffffffu, st, nb);
+            ce = __shfl_sync(0xffffffffu, en, nb);
+          }
+        }
+      }
+      if (fill == 0) break;
+      __syncwarp();
+      if (mine) {
+        for (int t0 = 0; t0 < fill; t0 += 4) {
+          bool in[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            in[u] = t0 + u < fill && member(tile[wib][t0 + u], cx, cy, cz, rad2);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (in[u]) {
+              if (FILL) {
+                const int j = tid_[wib][t0 + u];
+                if (row) row[k] = j;
+                const int e = k & 3;
+                if (e == 0) pend.x = j;
+                else if (e == 1) pend.y = j;
+                else if (e == 2) pend.z = j;
+                else {
+                  pend.w = j;
+                  if (sblk) sblk[32 * (k >> 2)] = pend;   // one 16-byte store per 4 entries
+                }
+              }
+              ++k;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      fill = 0;
+      if (nb >= 27) break;
+    }
+  }
+  if (FILL && sblk && (k & 3)) sblk[32 * (k >> 2)] = pend;     // partial last block
+  if (!FILL && valid) cnt[g] = k;
+}
+
+// CSR rows from the SELL-32x4 copy (thread per row; materialised on demand)
+__global__ void sell_to_csr_kernel(const int64_t* __restrict__ nptr, int64_t n_rows,
+                                   const int64_t* __restrict__ sptr,
+                                   const int32_t* __restrict__ sidx, int32_t* __restrict__ nidx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const int64_t b = nptr[r], len = nptr[r + 1] - b;
+  const int4* blk = reinterpret_cast<const int4*>(sidx + sptr[r >> 5]) + (r & 31);
+  for (int64_t i = 0; i < len; i += 4) {
+    const int4 v = blk[32 * (i >> 2)];
+    nidx[b + i] = v.x;
+    if (i + 1 < len) nidx[b + i + 1] = v.y;
+    if (i + 2 < len) nidx[b + i + 2] = v.z;
+    if (i + 3 < len) nidx[b + i + 3] = v.w;
+  }
+}
+
 __global__ void set_tail(int64_t* cnt, int64_t n) { cnt[n] = 0; }
 
 // one warp per 32-row slice: width = longest row; writes 32 * width (slice entries)
@@ -511,7 +663,7 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     tb = L.tmp_bytes;
     cub::DeviceRadixSort::SortPairs(tmp, tb, ckey_in, ckey, cval_in, ctr_order, (int)n_ctr, 0,
                                     3 * kFineBits, st);
-    sweep_thread_kernel<false><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+    sweep_cell_kernel<false><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
         ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, cnt, nullptr,
         nullptr, nullptr, nullptr);
   }
@@ -547,7 +699,7 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     return set_error(TSQBX_ERR_ARGUMENT, "near_fill: workspace too small");
   if (n_ctr == 0) return TSQBX_OK;
   char* ws = static_cast<char*>(workspace);
-  sweep_thread_kernel<true><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+  sweep_cell_kernel<true><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
       ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
       reinterpret_cast<const double4*>(ws + L.off_sxyz),
       reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
@@ -633,6 +785,16 @@ int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near
   sell_fill_kernel<<<(int)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       near_ptr, near_idx, n_rows, sell_ptr, sell_idx);
   return check_cuda(cudaGetLastError(), "sell_fill launch");
+}
+
+int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,
+                      const int32_t* sell_idx, int32_t* near_idx, void* stream) {
+  if (n_rows < 0 || (n_rows > 0 && (!near_ptr || !sell_ptr || !sell_idx || !near_idx)))
+    return set_error(TSQBX_ERR_ARGUMENT, "sell_to_csr: bad arguments");
+  if (n_rows == 0) return TSQBX_OK;
+  sell_to_csr_kernel<<<(int)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      near_ptr, n_rows, sell_ptr, sell_idx, near_idx);
+  return check_cuda(cudaGetLastError(), "sell_to_csr launch");
 }
 
 int tsqbx_scatter_c128(int64_t n, const int64_t* dest, const double* src, double* out,

@@ -41,11 +41,26 @@ class NearLists:
     n_src: int
     n_pairs: int
     ptr: torch.Tensor
-    idx: torch.Tensor
+    csr_idx: torch.Tensor | None          # CSR entries; None until first needed
     src_perm: torch.Tensor | None = None
     ctr_order: torch.Tensor | None = None
     sell_ptr: torch.Tensor | None = None
     sell_idx: torch.Tensor | None = None
+
+    @property
+    def idx(self) -> torch.Tensor:
+        """CSR entries (materialised from the SELL copy on first use: the fast
+        kernels read only the SELL layout)."""
+        if self.csr_idx is None:
+            L = _lib.load()
+            dev = self.ptr.device
+            out = torch.empty(max(self.n_pairs, 1), dtype=torch.int32, device=dev)
+            _lib.check(L.tsqbx_sell_to_csr(self.n_ctr, self.ptr.data_ptr(),
+                                           self.sell_ptr.data_ptr(), self.sell_idx.data_ptr(),
+                                           out.data_ptr(), dv.stream_handle(dev)),
+                       "tsqbx_sell_to_csr")
+            self.csr_idx = out[:self.n_pairs]
+        return self.csr_idx
 
     @property
     def mean_len(self) -> float:
@@ -86,7 +101,7 @@ class NearLists:
         i = dv.to_device(idx, torch.int32, dev)
         n_ctr = int(p.shape[0]) - 1
         n_pairs = int(i.shape[0])
-        return cls(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=p, idx=i)
+        return cls(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=p, csr_idx=i)
 
     def to_user_csr(self) -> tuple[np.ndarray, np.ndarray]:
         """(ptr, idx) on the host with rows by user center and user source indices."""
@@ -141,12 +156,14 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
                                   ctr_order.data_ptr(), nptr.data_ptr(), dv.ptr(sptr),
                                   totals.data_ptr(), st), "tsqbx_near_count")
     n_pairs, n_sell = (int(v) for v in totals.cpu().tolist())
-    idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
+    # with the SELL copy only it is written; the CSR entries are derived on demand
+    idx = None if sell else torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
     sidx = torch.empty(max(n_sell, 4), dtype=torch.int32, device=dev) if sell else None
     _lib.check(L.tsqbx_near_fill(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
                                  ws.data_ptr(), ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
-                                 idx.data_ptr(), dv.ptr(sptr), dv.ptr(sidx), st),
+                                 dv.ptr(idx), dv.ptr(sptr), dv.ptr(sidx), st),
                "tsqbx_near_fill")
-    return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr, idx=idx[:n_pairs],
+    return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr,
+                     csr_idx=None if idx is None else idx[:n_pairs],
                      src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],
                      sell_ptr=sptr, sell_idx=sidx)

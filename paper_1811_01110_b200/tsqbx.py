@@ -145,10 +145,13 @@ class _Prepared:
         sell = self.layout == "sell" and near.sell_ptr is not None
         if sell and g0 % 32:
             raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
+        # the fast S kernels read only the SELL copy; the others need the CSR entries
+        fast = self.variant == 0 and self.cfg.p_qbx <= 16 and not generic
+        csr = None if (sell and fast) else near.idx
         _lib.check(L.tsqbx_eval_packed(
             self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,
             self.with_normals, self.ctr.data_ptr() + 24 * g0, g1 - g0,
-            near.ptr.data_ptr() + 8 * g0, near.idx.data_ptr(),
+            near.ptr.data_ptr() + 8 * g0, dv.ptr(csr),
             near.sell_ptr.data_ptr() + 8 * (g0 // 32) if sell else None,
             near.sell_idx.data_ptr() if sell else None, self.tgt.data_ptr(),
             dv.ptr(self.tn), self.tptr.data_ptr() + 8 * g0, self.n_tgt,
@@ -359,7 +362,7 @@ def ts_accumulate(cfg: TsConfig, sources, weights, center, target,
                                        dev)
     near = NearLists(n_ctr=1, n_src=n, n_pairs=n,
                      ptr=torch.tensor([0, n], dtype=torch.int64, device=dev),
-                     idx=torch.arange(n, dtype=torch.int32, device=dev))
+                     csr_idx=torch.arange(n, dtype=torch.int32, device=dev))
     tptr = torch.tensor([0, 1], dtype=torch.int64, device=dev)
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr)
     out = torch.empty(1, dtype=torch.complex128, device=dev)

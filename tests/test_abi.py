@@ -91,7 +91,8 @@ def test_near_lists_user_export_roundtrip():
     idx = torch.tensor([0, 1, 2, 0, 1, 2], dtype=torch.int32)
     perm = torch.tensor([2, 0, 1], dtype=torch.int32)
     order = torch.tensor([3, 1, 0, 2], dtype=torch.int32)
-    nl = NearLists(n_ctr=4, n_src=3, n_pairs=6, ptr=ptr, idx=idx, src_perm=perm, ctr_order=order)
+    nl = NearLists(n_ctr=4, n_src=3, n_pairs=6, ptr=ptr, csr_idx=idx, src_perm=perm,
+                   ctr_order=order)
     uptr, uidx = nl.to_user_csr()
     assert uptr.tolist() == [0, 0, 1, 4, 6]
     rows = [uidx[uptr[c]:uptr[c + 1]].tolist() for c in range(4)]
