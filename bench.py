@@ -343,7 +343,7 @@ def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
     spec = case.cfg.spec
     fpp = configs.algorithmic_flops_per_pair(spec, case.cfg.p_qbx)
     mean_ms = sum(ms) / len(ms)
-    launches_per_step = 1 if spec.is_laplace else 2
+    launches_per_step = 1   # one evaluation kernel (Helmholtz SELL computes j_n in-kernel)
     # SURVEY.md 8(d) compulsory bytes: sources 40 B, centers 32 B, 4 B per CSR entry,
     # targets 48 B (coordinates, output slot, potential)
     alg_bytes = (case.n_sources * 40 + case.n_centers * 32 + near.n_pairs * 4

@@ -333,6 +333,9 @@ constexpr int kSellBlock = 128;   // threads per CTA of the SELL kernels
 #ifndef TSQBX_HELM_MINB
 #define TSQBX_HELM_MINB 4
 #endif
+#ifndef TSQBX_LAP_UNROLL2
+#define TSQBX_LAP_UNROLL2 0
+#endif
 #ifndef TSQBX_HELM_CF_SMEM
 #define TSQBX_HELM_CF_SMEM 0
 #endif
@@ -408,10 +411,8 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       ar[q] = ai[q] = bm[q] = 0.0;
     }
     SellStream ss(a, g, len, REALW, ring);
-    while (ss.more()) {
-      double4 q4;
-      double wim;
-      ss.next(q4, wim);
+    // one source against the NT targets
+    auto source = [&](const double4& q4, double wim) {
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
       const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
       const double iR = rsqrt_fast(R2);
@@ -427,7 +428,31 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
         if (!REALW) ai[q] = fma(S, wi, ai[q]);
         if (VAL) bm[q] = fmax(bm[q], B);
       }
+    };
+#if TSQBX_LAP_UNROLL2
+    // two sources per trip: independent dependency chains for the scheduler; an
+    // odd tail pairs with a zero-weight dummy one unit away (finite, adds 0)
+    while (ss.more()) {
+      double4 qa, qb;
+      double wa, wb;
+      ss.next(qa, wa);
+      if (ss.more()) {
+        ss.next(qb, wb);
+      } else {
+        qb = make_double4(cx + 1.0, cy, cz, 0.0);
+        wb = 0.0;
+      }
+      source(qa, wa);
+      source(qb, wb);
     }
+#else
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      source(q4, wim);
+    }
+#endif
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
@@ -486,9 +511,20 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_HELM_MINB) helmholtz_sell_ke
       tx[q] = ux * ir;
       ty[q] = uy * ir;
       tz[q] = uz * ir;
+      // c_n = (2n+1) j_n(k r) kappa_n computed here, in registers (no table pass);
+      // j_n(0) = delta_n0 (_core.pyx:357)
+      {
+        double jn[P + 1];
+        const double rr = r2[q] * ir;                 // |t - c|
+        if (ok && rr > 0.0) {
+          miller_j_reg<P + 1>(k * rr, jn);
+        } else {
 #pragma unroll
-      for (int n = 0; n <= P; ++n)
-        CF(n, q) = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
+          for (int n = 0; n <= P; ++n) jn[n] = n == 0 && ok ? 1.0 : 0.0;
+        }
+#pragma unroll
+        for (int n = 0; n <= P; ++n) CF(n, q) = (2.0 * n + 1.0) * jn[n] * c_leg.kappa[n];
+      }
       ar[q] = ai[q] = bm[q] = 0.0;
     }
     SellStream ss(a, g, len, false, ring);
@@ -1028,9 +1064,11 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
     if (!workspace || ws_bytes < need)
       return set_error(TSQBX_ERR_ARGUMENT, "workspace too small: need %lld bytes", (long long)need);
     a.ttab = static_cast<const double*>(workspace);
-    helmholtz_target_table<<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
-        ctr_xyz, n_ctr, tgt_xyz, tgt_ptr, p, k, fast ? 0 : 1, static_cast<double*>(workspace),
-        a.ttab_stride);
+    // the SELL fast kernel computes its targets' Bessel coefficients itself
+    if (!(fast && sell_ptr))
+      helmholtz_target_table<<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+          ctr_xyz, n_ctr, tgt_xyz, tgt_ptr, p, k, fast ? 0 : 1, static_cast<double*>(workspace),
+          a.ttab_stride);
   }
   if (fast) {
     const int nt = n_tgt >= 2 * n_ctr ? 2 : 1;
