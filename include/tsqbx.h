@@ -53,6 +53,7 @@ extern "C" {
 #define TSQBX_FLAG_VALIDATE 1u   /* cheap in-kernel screening, see tsqbx_validate */
 #define TSQBX_FLAG_GENERIC 2u    /* force the runtime-p reference-order kernel */
 #define TSQBX_FLAG_REAL_WEIGHTS 4u /* caller guarantees Im w == 0: skip the imaginary part */
+#define TSQBX_FLAG_ONE_TARGET 8u   /* fast kernels: one target per pass (fewer registers) */
 
 #define TSQBX_MAX_ORDER 64
 

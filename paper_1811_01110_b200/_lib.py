@@ -32,6 +32,7 @@ EQ_HELMHOLTZ = 1
 FLAG_VALIDATE = 1
 FLAG_GENERIC = 2
 FLAG_REAL_WEIGHTS = 4
+FLAG_ONE_TARGET = 8
 MAX_ORDER = 64
 ERR_KEY_NONE = (1 << 63) - 1
 ERR_KEY_SUSPECT = (1 << 63) - 2

@@ -1071,7 +1071,7 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
           a.ttab_stride);
   }
   if (fast) {
-    const int nt = n_tgt >= 2 * n_ctr ? 2 : 1;
+    const int nt = (n_tgt >= 2 * n_ctr && !(flags & TSQBX_FLAG_ONE_TARGET)) ? 2 : 1;
     FastOrders::run(p, equation, sell_ptr != nullptr, nt, val, a, n_ctr, st);
   } else {
     const int blocks = (int)((n_ctr * G + 127) / 128);

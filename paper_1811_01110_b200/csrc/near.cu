@@ -434,30 +434,20 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
   int4* sblk = (FILL && valid && sidx) ? reinterpret_cast<int4*>(sidx + sptr[g >> 5]) + (g & 31)
                                        : nullptr;
   int4 pend = make_int4(0, 0, 0, 0);   // entries of the current SELL block not yet stored
-  const unsigned long long prev = __shfl_up_sync(0xffffffffu, ckey, 1);
-  unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || prev != ckey));
   int k = 0;
-  while (heads) {
-    const int a = __ffs(heads) - 1;
-    heads &= heads - 1;
-    const unsigned long long cell = __shfl_sync(0xffffffffu, ckey, a);
-    const unsigned long long bx = __shfl_sync(0xffffffffu, ccx, a);
-    const unsigned long long by = __shfl_sync(0xffffffffu, ccy, a);
-    const unsigned long long bz = __shfl_sync(0xffffffffu, ccz, a);
-    const bool mine = valid && ckey == cell;
-    int st = 0, en = 0;
-    if (lane < 27) {
-      const unsigned long long nk =
-          morton3(bx + (lane / 9) - 1, by + ((lane / 3) % 3) - 1, bz + (lane % 3) - 1);
-      if (!hash_find(hkey, hst, hen, cap, nk, st, en)) en = st;
-    }
-    // walk the neighbour cells in order, filling the tile; flush when full
-    int fill = 0;            // candidates staged in the tile
-    int nb = 0, pos = 0;     // next neighbour cell and position inside it
-    int cs = __shfl_sync(0xffffffffu, st, 0), ce = __shfl_sync(0xffffffffu, en, 0);
+  // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
+  // c % 32, slot c / 32) through the tile; lanes with `mine` test them all.
+  auto run_cells = [&](int ncell, int stA, int enA, int stB, int enB, bool mine) {
+    auto range = [&](int c, int& cs, int& ce) {
+      const int s0 = __shfl_sync(0xffffffffu, stA, c & 31), e0 = __shfl_sync(0xffffffffu, enA, c & 31);
+      const int s1 = __shfl_sync(0xffffffffu, stB, c & 31), e1 = __shfl_sync(0xffffffffu, enB, c & 31);
+      cs = c < 32 ? s0 : s1;
+      ce = c < 32 ? e0 : e1;
+    };
+    int fill = 0, nb = 0, pos = 0, cs, ce;
+    range(0, cs, ce);
     while (true) {
-      // stage candidates until the tile is full or every neighbour is done
-      while (nb < 27 && fill < kTile) {
+      while (nb < ncell && fill < kTile) {        // stage until the tile is full
         const int take = min(ce - (cs + pos), kTile - fill);
         for (int q = lane; q < take; q += 32) {
           const int j = cs + pos + q;
@@ -469,10 +459,7 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
         if (cs + pos >= ce) {
           ++nb;
           pos = 0;
-          if (nb < 27) {
-            cs = __shfl_sync(0xffffffffu, st, nb);
-            ce = __shfl_sync(0xffffffffu, en, nb);
-          }
+          if (nb < ncell) range(nb, cs, ce);
         }
       }
       if (fill == 0) break;
@@ -505,7 +492,55 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
       }
       __syncwarp();
       fill = 0;
-      if (nb >= 27) break;
+      if (nb >= ncell) break;
+    }
+  };
+  auto lookup = [&](unsigned long long x, unsigned long long y, unsigned long long z, int& st,
+                    int& en) {
+    st = en = 0;
+    if (!hash_find(hkey, hst, hen, cap, morton3(x, y, z), st, en)) en = st;
+  };
+  // Union mode: when the warp's centers sit in a small block of cells, every
+  // lane scans the union of their neighbourhoods at once (all lanes busy);
+  // candidates outside a lane's own 27 cells simply fail the distance test.
+  unsigned long long lo[3] = {valid ? ccx : ~0ull, valid ? ccy : ~0ull, valid ? ccz : ~0ull};
+  unsigned long long hi[3] = {valid ? ccx : 0ull, valid ? ccy : 0ull, valid ? ccz : 0ull};
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = min(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], off));
+      hi[d] = max(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], off));
+    }
+  }
+  const unsigned long long ex = hi[0] - lo[0] + 3, ey = hi[1] - lo[1] + 3, ez = hi[2] - lo[2] + 3;
+  if (ex * ey * ez <= 64) {
+    const int ncell = (int)(ex * ey * ez);
+    int stA = 0, enA = 0, stB = 0, enB = 0;
+    for (int slot = 0; slot < 2; ++slot) {
+      const int c = lane + 32 * slot;
+      if (c < ncell) {
+        const unsigned long long ix = c / (ey * ez), iy = (c / ez) % ey, iz = c % ez;
+        int st, en;
+        lookup(lo[0] - 1 + ix, lo[1] - 1 + iy, lo[2] - 1 + iz, st, en);
+        if (slot == 0) { stA = st; enA = en; } else { stB = st; enB = en; }
+      }
+    }
+    run_cells(ncell, stA, enA, stB, enB, valid);
+  } else {
+    // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
+    const unsigned long long prev = __shfl_up_sync(0xffffffffu, ckey, 1);
+    unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || prev != ckey));
+    while (heads) {
+      const int a = __ffs(heads) - 1;
+      heads &= heads - 1;
+      const unsigned long long cell = __shfl_sync(0xffffffffu, ckey, a);
+      const unsigned long long bx = __shfl_sync(0xffffffffu, ccx, a);
+      const unsigned long long by = __shfl_sync(0xffffffffu, ccy, a);
+      const unsigned long long bz = __shfl_sync(0xffffffffu, ccz, a);
+      int st = 0, en = 0;
+      if (lane < 27) lookup(bx + (lane / 9) - 1, by + ((lane / 3) % 3) - 1, bz + (lane % 3) - 1, st, en);
+      run_cells(27, st, en, 0, 0, valid && ckey == cell);
     }
   }
   if (FILL && sblk && (k & 3)) sblk[32 * (k >> 2)] = pend;     // partial last block

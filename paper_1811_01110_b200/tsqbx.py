@@ -131,6 +131,7 @@ class _Prepared:
         # real Laplace densities: the pack kernel flags any Im w != 0 on the device
         # and the kernel picks its real-weight path itself (no host round trip)
         self.real_w = False
+        self.one_target = os.environ.get("GIGAQBX_ONE_TARGET", "0") == "1"
 
     def launch(self, out: torch.Tensor, validate: bool, generic: bool = False,
                rows: tuple[int, int] | None = None, out_offset: int = 0,
@@ -139,7 +140,8 @@ class _Prepared:
         (multi-GPU shard); ``user_order=False`` writes processing order."""
         L = _lib.load()
         flags = ((_lib.FLAG_VALIDATE if validate else 0) | (_lib.FLAG_GENERIC if generic else 0)
-                 | (_lib.FLAG_REAL_WEIGHTS if self.real_w else 0))
+                 | (_lib.FLAG_REAL_WEIGHTS if self.real_w else 0)
+                 | (_lib.FLAG_ONE_TARGET if self.one_target else 0))
         near = self.near
         g0, g1 = rows if rows is not None else (0, self.n_ctr)
         sell = self.layout == "sell" and near.sell_ptr is not None
