@@ -148,7 +148,7 @@ class _Prepared:
         if sell and g0 % 32:
             raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
         # the fast S kernels read only the SELL copy; the others need the CSR entries
-        fast = self.variant == 0 and self.cfg.p_qbx <= 16 and not generic
+        fast = self.cfg.p_qbx <= 16 and not generic
         csr = None if (sell and fast) else near.idx
         _lib.check(L.tsqbx_eval_packed(
             self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,

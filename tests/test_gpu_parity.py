@@ -364,3 +364,35 @@ def test_full_size_properties_c2_dense():
                       case.targets, near_p, tgt_ptr=case.tgt_ptr)
     assert normwise(p4.evaluate().cpu().numpy(), u1.cpu().numpy()) <= 1e-13
     assert np.all(np.isfinite(u1.cpu().numpy()))
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 5, 8, 12, 16, 20])
+@pytest.mark.parametrize("eq", ["laplace", "helmholtz"])
+def test_derivative_variants_all_orders(p, eq):
+    """S' and D through the compile-time-order SELL kernels (p <= 16) and the
+    generic kernel (p = 20), including targets AT their center (r = 0
+    conventions, _core.pyx:262-264, 285-288, 357-359, 400-408)."""
+    rng = np.random.default_rng(100 + p)
+    n_src, n_ctr = 400, 60
+    src = rng.normal(size=(n_src, 3)) * 0.4 + np.array([0.0, 0.0, 2.0])
+    sn = rng.normal(size=(n_src, 3))
+    sn /= np.linalg.norm(sn, axis=1)[:, None]
+    w = rng.normal(size=n_src) + 1j * rng.normal(size=n_src)
+    ctr = rng.normal(size=(n_ctr, 3)) * 0.05
+    tptr = np.arange(0, 2 * n_ctr + 1, 2)
+    tgt = np.repeat(ctr, 2, axis=0) + rng.normal(size=(2 * n_ctr, 3)) * 0.05
+    tgt[::6] = ctr[::3]                              # every third center: a target at r = 0
+    tn = rng.normal(size=(2 * n_ctr, 3))
+    tn /= np.linalg.norm(tn, axis=1)[:, None]
+    lens = rng.integers(5, 40, size=n_ctr)
+    nptr = np.concatenate([[0], np.cumsum(lens)])
+    nidx = rng.integers(0, n_src, size=nptr[-1]).astype(np.int32)
+    for variant in (Variant.TARGET_NORMAL_DERIV, Variant.SOURCE_NORMAL_DERIV):
+        spec = KernelSpec(equation=Equation(eq), variant=variant,
+                          helmholtz_k=None if eq == "laplace" else 2.3)
+        cfg = TsConfig(spec, p)
+        out = ts_accumulate_batch(cfg, src, w, ctr, tgt, (nptr, nidx), tgt_ptr=tptr,
+                                  source_normals=sn, target_normals=tn)
+        ref = oracle.ts_batch(eq, spec.variant_code, spec.helmholtz_k or 0.0, p, src, w, ctr,
+                              nptr, nidx, tgt, tptr, snormals=sn, tnormals=tn)
+        assert normwise(out, ref) <= (LAP_TOL if eq == "laplace" else HELM_TOL), (variant, p)

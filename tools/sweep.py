@@ -19,14 +19,26 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--peak", type=float, default=35.77)
 a = ap.parse_args()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+from paper_1811_01110_b200 import KernelSpec, TsConfig  # noqa: E402
+from paper_1811_01110_b200.kernels import Variant  # noqa: E402
+
+VAR = {"s": Variant.SINGLE_LAYER, "sp": Variant.TARGET_NORMAL_DERIV, "d": Variant.SOURCE_NORMAL_DERIV}
 for cs in a.cases.split(","):
-    name, preset = cs.split("/")
+    parts = cs.split("/")
+    name, preset = parts[0], parts[1]
     case = configs.make_case(name, preset)
+    if len(parts) > 2:
+        sp = case.cfg.spec
+        case.cfg = TsConfig(KernelSpec(equation=sp.equation, variant=VAR[parts[2]],
+                                       helmholtz_k=sp.helmholtz_k), case.cfg.p_qbx)
+    import numpy as np  # noqa: E402
+    tnrm = np.repeat(case.normals, np.diff(case.tgt_ptr), axis=0)
     near = build_near_lists(case.centers, case.sources, case.near_radii)
     fpp = configs.algorithmic_flops_per_pair(case.cfg.spec, case.cfg.p_qbx)
     for G in [int(x) for x in a.lanes.split(",")]:
         prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets,
-                            near, tgt_ptr=case.tgt_ptr, group_lanes=G or None)
+                            near, tgt_ptr=case.tgt_ptr, group_lanes=G or None,
+                            source_normals=case.normals, target_normals=tnrm)
         pairs = prob.pair_count()
         for _ in range(3):
             prob.evaluate()
