@@ -17,6 +17,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -325,13 +326,22 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
 // kRing index blocks (4 entries each) are in flight ahead of use, so the
 // DRAM latency of the CSR stream never reaches the arithmetic.  The source
 // record (an L1/L2 gather) is fetched one entry ahead into registers.
-constexpr int kSellBlock = 128;   // threads per CTA of the SELL kernels
+#ifndef TSQBX_SELL_BLOCK
+#define TSQBX_SELL_BLOCK 256
+#endif
+#ifndef TSQBX_RING
+#define TSQBX_RING 3
+#endif
+#ifndef TSQBX_PERSIST
+#define TSQBX_PERSIST 0
+#endif
+constexpr int kSellBlock = TSQBX_SELL_BLOCK;   // threads per CTA of the SELL kernels
 // minimum resident CTAs per SM requested from ptxas (caps registers per thread)
 #ifndef TSQBX_LAP_MINB
-#define TSQBX_LAP_MINB 6
+#define TSQBX_LAP_MINB 3
 #endif
 #ifndef TSQBX_HELM_MINB
-#define TSQBX_HELM_MINB 4
+#define TSQBX_HELM_MINB 2
 #endif
 #ifndef TSQBX_LAP_UNROLL2
 #define TSQBX_LAP_UNROLL2 0
@@ -339,7 +349,8 @@ constexpr int kSellBlock = 128;   // threads per CTA of the SELL kernels
 #ifndef TSQBX_HELM_CF_SMEM
 #define TSQBX_HELM_CF_SMEM 0
 #endif
-constexpr int kRing = 4;          // index blocks in flight (16 entries of lookahead)
+constexpr int kRing = TSQBX_RING;  // index blocks in flight (4 kRing entries of lookahead)
+constexpr int kSlots = kRing + 1;  // ring slots per thread (a power of two keeps b % kSlots a mask)
 
 template <bool NRM = false>
 struct SellStream {
@@ -356,8 +367,8 @@ struct SellStream {
   double4 n_next;
 
   __device__ __forceinline__ void issue(int b) {
-    // block b goes to slot b % (kRing + 1); always commit so group counts stay uniform
-    if (b < nblk) cp_async16(ring + (b % (kRing + 1)) * kSellBlock, blk + 32 * b);
+    // block b goes to slot b % kSlots; always commit so group counts stay uniform
+    if (b < nblk) cp_async16(ring + (b % kSlots) * kSellBlock, blk + 32 * b);
     cp_async_commit();
   }
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t g, int n, bool realw,
@@ -375,7 +386,7 @@ struct SellStream {
   }
   __device__ __forceinline__ void enter_block(int b) {
     cp_async_wait<kRing - 1>();                 // block b has landed
-    cur = ring[(b % (kRing + 1)) * kSellBlock];
+    cur = ring[(b % kSlots) * kSellBlock];
     issue(b + kRing);                           // reuses the slot of block b - 1
   }
   __device__ __forceinline__ void fetch(int s) {
@@ -477,13 +488,15 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
 // pack kernel records whether any Im w is nonzero, so no host round trip decides
 template <int P, int NT, bool VAL>
 __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
-  __shared__ int4 ring[(kRing + 1) * kSellBlock];
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.n_ctr) return;
-  if (a.real_w || *a.imag_flag == 0u)
-    laplace_sell_body<P, NT, VAL, true>(a, g, ring);
-  else
-    laplace_sell_body<P, NT, VAL, false>(a, g, ring);
+  __shared__ int4 ring[kSlots * kSellBlock];
+  const bool realw = a.real_w || *a.imag_flag == 0u;
+  const int64_t stride = TSQBX_PERSIST ? (int64_t)gridDim.x * blockDim.x : a.n_ctr;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ctr; g += stride) {
+    if (realw)
+      laplace_sell_body<P, NT, VAL, true>(a, g, ring);
+    else
+      laplace_sell_body<P, NT, VAL, false>(a, g, ring);
+  }
 }
 
 template <int P, int NT, bool VAL>
@@ -497,9 +510,9 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_HELM_MINB) helmholtz_sell_ke
   double cfr[NT][P + 1];
 #define CF(n, q) cfr[q][n]
 #endif
-  __shared__ int4 ring[(kRing + 1) * kSellBlock];
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.n_ctr) return;
+  __shared__ int4 ring[kSlots * kSellBlock];
+  const int64_t stride = TSQBX_PERSIST ? (int64_t)gridDim.x * blockDim.x : a.n_ctr;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ctr; g += stride) {
   const int tid = threadIdx.x;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
@@ -598,6 +611,7 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_HELM_MINB) helmholtz_sell_ke
       }
     }
   }
+}  // rows
 }
 #undef CF
 
@@ -629,8 +643,8 @@ struct Bonnet {
 static __constant__ Bonnet c_bon = Bonnet();
 
 template <int P, int NT, int VARIANT>
-__global__ void __launch_bounds__(kSellBlock, 4) laplace_deriv_sell_kernel(const EvalParams a) {
-  __shared__ int4 ring[(kRing + 1) * kSellBlock];
+__global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_sell_kernel(const EvalParams a) {
+  __shared__ int4 ring[kSlots * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.n_ctr) return;
   const bool val = a.validate != 0;
@@ -747,10 +761,10 @@ __global__ void __launch_bounds__(kSellBlock, 4) laplace_deriv_sell_kernel(const
 }
 
 template <int P, int NT, int VARIANT>
-__global__ void __launch_bounds__(kSellBlock, 3) helmholtz_deriv_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSellBlock : 1)) helmholtz_deriv_sell_kernel(const EvalParams a) {
   // per-thread target coefficients in (dynamic) shared memory, [term][n][q][thread]
   extern __shared__ double cfs[];
-  __shared__ int4 ring[(kRing + 1) * kSellBlock];
+  __shared__ int4 ring[kSlots * kSellBlock];
 #define CFA(n, q) cfs[((n) * NT + (q)) * kSellBlock + tid]
 #define CFB(n, q) cfs[(((P + 1) + (n)) * NT + (q)) * kSellBlock + tid]
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1217,13 +1231,25 @@ __global__ void pack_kernel(int64_t n, const double* __restrict__ xyz,
 // ---------------------------------------------------------------------------
 constexpr int kMaxFastOrder = 16;
 
+// CTAs of `kernel` (kSellBlock threads) resident at once on this device
+template <class K>
+int resident_blocks(K kernel) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSellBlock, 0);
+  return std::max(1, per_sm) * std::max(1, sms);
+}
+
 template <int P, int NT, bool VAL>
 void launch_fast(int equation, bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
   if (sell) {
-    const int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
+    int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
     if (equation == TSQBX_EQ_LAPLACE) {
+      if (TSQBX_PERSIST) blocks = std::min(blocks, resident_blocks(laplace_sell_kernel<P, NT, VAL>));
       laplace_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     } else {
+      if (TSQBX_PERSIST) blocks = std::min(blocks, resident_blocks(helmholtz_sell_kernel<P, NT, VAL>));
       helmholtz_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     }
     return;
