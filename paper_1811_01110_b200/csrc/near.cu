@@ -465,25 +465,29 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
       if (fill == 0) break;
       __syncwarp();
       if (mine) {
-        for (int t0 = 0; t0 < fill; t0 += 4) {
-          bool in[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            in[u] = t0 + u < fill && member(tile[wib][t0 + u], cx, cy, cz, rad2);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (in[u]) {
-              if (FILL) {
-                const int j = tid_[wib][t0 + u];
-                if (row) row[k] = j;
-                const int e = k & 3;
-                if (e == 0) pend.x = j;
-                else if (e == 1) pend.y = j;
-                else if (e == 2) pend.z = j;
-                else {
-                  pend.w = j;
-                  if (sblk) sblk[32 * (k >> 2)] = pend;   // one 16-byte store per 4 entries
-                }
+        // test 32 staged candidates into a per-lane bit mask, then append only
+        // this lane's members (no per-candidate divergent work in the fill)
+        for (int t0 = 0; t0 < fill; t0 += 32) {
+          const int m = min(32, fill - t0);
+          unsigned bits = 0u;
+#pragma unroll 8
+          for (int u = 0; u < 32; ++u)
+            if (u < m && member(tile[wib][t0 + u], cx, cy, cz, rad2)) bits |= 1u << u;
+          if (!FILL) {
+            k += __popc(bits);
+          } else {
+            while (bits) {
+              const int u = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int j = tid_[wib][t0 + u];
+              if (row) row[k] = j;
+              const int e = k & 3;
+              if (e == 0) pend.x = j;
+              else if (e == 1) pend.y = j;
+              else if (e == 2) pend.z = j;
+              else {
+                pend.w = j;
+                if (sblk) sblk[32 * (k >> 2)] = pend;   // one 16-byte store per 4 entries
               }
               ++k;
             }
