@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 3
+#define TSQBX_ABI_VERSION 4
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -54,6 +54,7 @@ extern "C" {
 #define TSQBX_FLAG_GENERIC 2u    /* force the runtime-p reference-order kernel */
 #define TSQBX_FLAG_REAL_WEIGHTS 4u /* caller guarantees Im w == 0: skip the imaginary part */
 #define TSQBX_FLAG_ONE_TARGET 8u   /* fast kernels: one target per pass (fewer registers) */
+#define TSQBX_FLAG_PRECISE 16u     /* p2p: IEEE 1/sqrt (after a non-finite screen with no singular pair) */
 
 #define TSQBX_MAX_ORDER 64
 
@@ -206,6 +207,47 @@ int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* se
  * all-gathered shards into user target order. */
 int tsqbx_scatter_c128(int64_t n, const int64_t* dest, const double* src, double* out,
                        void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Point-to-point direct interactions: replaces the
+ * reference backends' laplace_p2p / helmholtz_p2p (_core.pyx:94-165), called by
+ * kernels.direct_sum (kernels.py:114-136) and per target box by
+ * driver.direct_stage (driver.py:187-210).
+ *
+ *   out[t] = sum_j w_j K(t, s_j),  K = 1/(4 pi r) | e^{ikr}/(4 pi r) (S),
+ *            its target-normal (S') or source-normal (D) derivative.
+ *
+ * Dense (row_ptr NULL): every target sees every source.  Rows: row r's
+ * targets [row_tgt[r], row_tgt[r+1]) (rows partition [0, n_tgt) in order) see
+ * the packed sources row_idx[row_ptr[r] .. row_ptr[r+1]).
+ * With TSQBX_FLAG_VALIDATE a non-finite result sets *err_key to
+ * TSQBX_ERR_KEY_SUSPECT; tsqbx_p2p_find_singular then sets the exact key
+ * (target << 32) | source of the first target-major pair with r2 == 0 (the
+ * reference's "singular source/target pair: target i, source j"), or leaves
+ * TSQBX_ERR_KEY_NONE, in which case the caller re-runs with TSQBX_FLAG_PRECISE.
+ * ------------------------------------------------------------------------- */
+int64_t tsqbx_p2p_workspace_bytes(int64_t n_src, int64_t n_tgt, int64_t n_rows, int dense);
+int tsqbx_p2p_packed(int equation, int variant, double k, const double* packed, int64_t n_src,
+                     int with_normals, int64_t n_rows, const int64_t* row_tgt,
+                     const int64_t* row_ptr, const int32_t* row_idx, const double* tgt_xyz,
+                     const double* tgt_nrm, int64_t n_tgt, unsigned flags, void* workspace,
+                     int64_t ws_bytes, double* out, int64_t* err_key, void* stream);
+int tsqbx_p2p_find_singular(const double* packed, int64_t n_src, int64_t n_rows,
+                            const int64_t* row_tgt, const int64_t* row_ptr,
+                            const int32_t* row_idx, const double* tgt_xyz, int64_t n_tgt,
+                            int64_t* err_key, void* stream);
+/* user layout (dense direct sum): sources xyz (n,3), weights complex128 (n,)
+ * interleaved, normals (n,3) for D / (m,3) for S'; the workspace holds the
+ * packed sources plus the chunk partial sums. */
+int64_t tsqbx_p2p_user_workspace_bytes(int variant, int64_t n_src, int64_t n_tgt);
+int tsqbx_p2p_laplace(int variant, const double* src_xyz, const double* src_w,
+                      const double* src_nrm, int64_t n_src, const double* tgt_xyz,
+                      const double* tgt_nrm, int64_t n_tgt, unsigned flags, void* workspace,
+                      int64_t ws_bytes, double* out, int64_t* err_key, void* stream);
+int tsqbx_p2p_helmholtz(int variant, double k, const double* src_xyz, const double* src_w,
+                        const double* src_nrm, int64_t n_src, const double* tgt_xyz,
+                        const double* tgt_nrm, int64_t n_tgt, unsigned flags, void* workspace,
+                        int64_t ws_bytes, double* out, int64_t* err_key, void* stream);
 
 /* ---------------------------------------------------------------------------
  * FP64 roofline probe: every thread runs 8 independent DFMA chains of `iters`

@@ -373,3 +373,87 @@ int64_t orc_near_csr(const double* ctr, const double* rad, int64_t n_ctr, const 
   free(ks);
   return total;
 }
+
+/* ------------------------------------------------------------------ */
+/* point-to-point direct sum (_core.pyx:94-165)                        */
+/* ------------------------------------------------------------------ */
+/* One target over its sources [jb, je) (sel == NULL) or sel[jb..je).  Returns
+ * the first singular source position (r2 == 0, :109-111 / :145-147) or -1. */
+static int64_t p2p_target(int equation, int variant, double k, const double* src,
+                          const double* w, const double* snrm, const int32_t* sel, int64_t jb,
+                          int64_t je, const double* t, const double* tn, double* out) {
+  double complex acc = 0.0;
+  for (int64_t q = jb; q < je; ++q) {
+    const int64_t j = sel ? (int64_t)sel[q] : q;
+    const double dx = t[0] - src[3 * j], dy = t[1] - src[3 * j + 1], dz = t[2] - src[3 * j + 2];
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    if (r2 == 0.0) return q;
+    const double r = sqrt(r2);
+    const double complex wj = w[2 * j] + I * w[2 * j + 1];
+    if (equation == 0) {                              /* :114-123 */
+      if (variant == 0) {
+        acc = acc + wj / (kFourPi * r);
+      } else if (variant == 1) {
+        const double dot = tn[0] * dx + tn[1] * dy + tn[2] * dz;
+        acc = acc - wj * dot / (kFourPi * r2 * r);
+      } else {
+        const double* sn = snrm + 3 * j;
+        const double dot = sn[0] * dx + sn[1] * dy + sn[2] * dz;
+        acc = acc + wj * dot / (kFourPi * r2 * r);
+      }
+    } else {                                          /* :150-160 */
+      const double complex phase = cos(k * r) + I * sin(k * r);
+      if (variant == 0) {
+        acc = acc + wj * phase / (kFourPi * r);
+      } else {
+        const double complex radial = phase * (I * k * r - 1.0) / (kFourPi * r2 * r);
+        if (variant == 1) {
+          const double dot = tn[0] * dx + tn[1] * dy + tn[2] * dz;
+          acc = acc + wj * dot * radial;
+        } else {
+          const double* sn = snrm + 3 * j;
+          const double dot = sn[0] * dx + sn[1] * dy + sn[2] * dz;
+          acc = acc - wj * dot * radial;
+        }
+      }
+    }
+  }
+  out[0] = creal(acc);
+  out[1] = cimag(acc);
+  return -1;
+}
+
+int orc_p2p(int equation, int variant, double k, const double* src, const double* w,
+            const double* snrm, int64_t n_src, const int64_t* row_tgt, const int64_t* row_ptr,
+            const int32_t* row_idx, int64_t n_rows, const double* tgt, const double* tnrm,
+            int64_t n_tgt, double* out, int64_t* bad, int nthreads) {
+  if (n_src < 0 || n_tgt < 0 || (variant == 1 && !tnrm) || (variant == 2 && !snrm)) return 2;
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+  const int dense = row_ptr == NULL;
+  if (dense) n_rows = 1;
+  unsigned long long first = ~0ull;
+#pragma omp parallel for schedule(dynamic, 16) reduction(min : first)
+  for (int64_t it = 0; it < n_tgt; ++it) {
+    /* the row owning target it (rows partition [0, n_tgt) in order) */
+    int64_t r = 0;
+    if (!dense) {
+      int64_t a = 0, b = n_rows;
+      while (b - a > 1) {
+        const int64_t m = (a + b) / 2;
+        if (row_tgt[m] <= it) a = m; else b = m;
+      }
+      r = a;
+    }
+    const int64_t jb = dense ? 0 : row_ptr[r], je = dense ? n_src : row_ptr[r + 1];
+    out[2 * it] = out[2 * it + 1] = 0.0;
+    const int64_t q = p2p_target(equation, variant, k, src, w, snrm, dense ? NULL : row_idx, jb,
+                                 je, tgt + 3 * it, tnrm ? tnrm + 3 * it : NULL, out + 2 * it);
+    if (q >= 0) {
+      const unsigned long long j = dense ? (unsigned long long)q : (unsigned long long)row_idx[q];
+      const unsigned long long key = ((unsigned long long)it << 32) | j;
+      if (key < first) first = key;
+    }
+  }
+  *bad = first == ~0ull ? -1 : (int64_t)first;
+  return first == ~0ull ? 0 : 1;
+}

@@ -56,3 +56,27 @@ def ts_accum_helmholtz(variant, k, p, sources, weights, snormals, center, target
     spec = KernelSpec(equation=Equation.HELMHOLTZ, variant=_VARIANTS[int(variant)],
                       helmholtz_k=float(k))
     return _one(spec, p, sources, weights, snormals, center, target, tnormal)
+
+
+def _p2p(spec, sources, weights, snormals, targets, tnormals):
+    from ..p2p import P2PProblem
+
+    targets = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros(targets.shape[0], dtype=np.complex128)
+    if np.asarray(sources).size == 0 or targets.shape[0] == 0:
+        return out
+    prob = P2PProblem(spec, sources, weights, snormals)
+    return prob.evaluate(targets, tnormals).cpu().numpy()
+
+
+def laplace_p2p(variant, sources, weights, snormals, targets, tnormals):
+    """_core.laplace_p2p (_core.pyx:94-125) on the GPU (same ValueError on r = 0)."""
+    spec = KernelSpec(equation=Equation.LAPLACE, variant=_VARIANTS[int(variant)])
+    return _p2p(spec, sources, weights, snormals, targets, tnormals)
+
+
+def helmholtz_p2p(variant, k, sources, weights, snormals, targets, tnormals):
+    """_core.helmholtz_p2p (_core.pyx:128-165) on the GPU."""
+    spec = KernelSpec(equation=Equation.HELMHOLTZ, variant=_VARIANTS[int(variant)],
+                      helmholtz_k=float(k))
+    return _p2p(spec, sources, weights, snormals, targets, tnormals)

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
                                                                "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
-ABI_VERSION = 3      # TSQBX_ABI_VERSION in include/tsqbx.h
+ABI_VERSION = 4      # TSQBX_ABI_VERSION in include/tsqbx.h
 
 # status codes (include/tsqbx.h)
 OK = 0
@@ -33,6 +33,7 @@ FLAG_VALIDATE = 1
 FLAG_GENERIC = 2
 FLAG_REAL_WEIGHTS = 4
 FLAG_ONE_TARGET = 8
+FLAG_PRECISE = 16
 MAX_ORDER = 64
 ERR_KEY_NONE = (1 << 63) - 1
 ERR_KEY_SUSPECT = (1 << 63) - 2
@@ -71,6 +72,14 @@ SIGNATURES = {
     "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_fp64_probe": (_I, [_P, _I64, _I, _I, _P]),
+    "tsqbx_p2p_workspace_bytes": (_I64, [_I64, _I64, _I64, _I]),
+    "tsqbx_p2p_packed": (_I, [_I, _I, _D, _P, _I64, _I, _I64, _P, _P, _P, _P, _P, _I64, _U, _P,
+                              _I64, _P, _P, _P]),
+    "tsqbx_p2p_find_singular": (_I, [_P, _I64, _I64, _P, _P, _P, _P, _I64, _P, _P]),
+    "tsqbx_p2p_user_workspace_bytes": (_I64, [_I, _I64, _I64]),
+    "tsqbx_p2p_laplace": (_I, [_I, _P, _P, _P, _I64, _P, _P, _I64, _U, _P, _I64, _P, _P, _P]),
+    "tsqbx_p2p_helmholtz": (_I, [_I, _D, _P, _P, _P, _I64, _P, _P, _I64, _U, _P, _I64, _P, _P,
+                                 _P]),
 }
 
 _lib = None

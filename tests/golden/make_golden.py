@@ -2,7 +2,7 @@
 
 Run in the build container (needs /root/reference; never at test time):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [name ...]     # default: all
 
 The reference package is imported read-only from /root/reference/pkg/src.
 Its backend selection falls back to the NumPy twin there (the compiled
@@ -125,18 +125,52 @@ def sphere_case(n, p, k, mult, off_surface, seed):
                 p=np.array(p), k=np.array(k or 0.0), value=out)
 
 
-def main():
-    np.savez_compressed(os.path.join(HERE, "pairs_p8.npz"), **pair_cases())
-    np.savez_compressed(os.path.join(HERE, "backend_batch.npz"), **backend_batch())
-    np.savez_compressed(os.path.join(HERE, "c1_literal.npz"),
-                        **sphere_case(4096, 4, None, 3.0, False, 0))
-    np.savez_compressed(os.path.join(HERE, "c2_small_literal.npz"),
-                        **sphere_case(2048, 8, None, 4.0, True, 1))
-    np.savez_compressed(os.path.join(HERE, "c3_small_literal.npz"),
-                        **sphere_case(2048, 8, 10.0, 4.0, True, 2))
+def p2p_cases():
+    """Direct sums through the reference's p2p backends (_core.pyx:94-165; the
+    compiled core and the NumPy twin must agree): test_backends.py:17-45 style
+    data (40 sources, 7 targets, k = 1.7) and a 300 x 200 random cloud, every
+    (equation, variant)."""
+    out = {}
+    rng = np.random.default_rng(11)
+    for tag, ns, nt in (("small", 40, 7), ("cloud", 300, 200)):
+        src = rng.normal(size=(ns, 3)) + np.array([0, 0, 3.0])
+        tgt = rng.normal(size=(nt, 3))
+        w = (rng.normal(size=ns) + 1j * rng.normal(size=ns)).astype(np.complex128)
+        sn = rng.normal(size=(ns, 3))
+        sn /= np.linalg.norm(sn, axis=1)[:, None]
+        tn = rng.normal(size=(nt, 3))
+        tn /= np.linalg.norm(tn, axis=1)[:, None]
+        out.update({f"{tag}_src": src, f"{tag}_tgt": tgt, f"{tag}_w": w, f"{tag}_snrm": sn,
+                    f"{tag}_tnrm": tn})
+        for v in range(3):
+            a = core.laplace_p2p(v, src, w, sn, tgt, tn)
+            b = core.helmholtz_p2p(v, 1.7, src, w, sn, tgt, tn)
+            a2 = ref_numpy.laplace_p2p(v, src, w, sn, tgt, tn)
+            b2 = ref_numpy.helmholtz_p2p(v, 1.7, src, w, sn, tgt, tn)
+            assert np.max(abs(a - a2)) <= 1e-13 * np.max(abs(a))
+            assert np.max(abs(b - b2)) <= 1e-13 * np.max(abs(b))
+            out[f"{tag}_laplace_{v}"] = a
+            out[f"{tag}_helmholtz_{v}"] = b
+    out["k"] = np.array(1.7)
+    return out
+
+
+GOLDEN = {
+    "pairs_p8": pair_cases,
+    "backend_batch": backend_batch,
+    "c1_literal": lambda: sphere_case(4096, 4, None, 3.0, False, 0),
+    "c2_small_literal": lambda: sphere_case(2048, 8, None, 4.0, True, 1),
+    "c3_small_literal": lambda: sphere_case(2048, 8, 10.0, 4.0, True, 2),
+    "p2p": p2p_cases,
+}
+
+
+def main(names):
+    for name in names or GOLDEN:
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), **GOLDEN[name]())
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

@@ -107,3 +107,69 @@ def test_reference_core_agrees_with_port():
                 a = core.ts_accum_helmholtz(v, 3.1, p, src, w, sn, np.zeros(3), t, tn)
                 b = oracle.ts_accum_helmholtz(v, 3.1, p, src, w, sn, np.zeros(3), t, tn)
                 assert normwise(b, a) <= 1e-14
+
+
+# ---- point-to-point direct sum (_core.pyx:94-165) ------------------------
+
+@pytest.mark.parametrize("tag", ["small", "cloud"])
+def test_p2p_golden(golden_dir, tag):
+    g = np.load(os.path.join(golden_dir, "p2p.npz"))
+    for v in range(3):
+        a = oracle.p2p("laplace", v, None, g[f"{tag}_src"], g[f"{tag}_w"], g[f"{tag}_tgt"],
+                       g[f"{tag}_snrm"], g[f"{tag}_tnrm"])
+        b = oracle.p2p("helmholtz", v, float(g["k"]), g[f"{tag}_src"], g[f"{tag}_w"],
+                       g[f"{tag}_tgt"], g[f"{tag}_snrm"], g[f"{tag}_tnrm"])
+        assert normwise(a, g[f"{tag}_laplace_{v}"]) <= 1e-15
+        assert normwise(b, g[f"{tag}_helmholtz_{v}"]) <= 1e-15
+
+
+def test_p2p_known_answers():
+    # test_kernels.py:18-22 (1/(4 pi) at unit distance), :102-105 (empty sources),
+    # :137-141 (Laplace, real weights: imaginary part exactly zero)
+    v = oracle.p2p("laplace", 0, None, [[0, 0, 0.0]], [1.0], [[1.0, 0, 0]])
+    assert v[0] == pytest.approx(1 / (4 * math.pi), rel=1e-15)
+    assert np.all(oracle.p2p("laplace", 0, None, np.zeros((0, 3)), [], np.ones((4, 3))) == 0)
+    rng = np.random.default_rng(3)
+    out = oracle.p2p("laplace", 0, None, rng.normal(size=(30, 3)), np.ones(30),
+                     rng.normal(size=(9, 3)) + 5)
+    assert np.all(out.imag == 0)
+
+
+def test_p2p_singular_pair_message():
+    # test_kernels.py:130-134: the first (target-major) coincident pair is named
+    src = np.array([[0, 0, 0.0], [1, 0, 0]])
+    tgt = np.array([[2, 0, 0.0], [1, 0, 0], [0, 0, 0]])
+    with pytest.raises(ValueError, match=r"singular source/target pair: target 1, source 1"):
+        oracle.p2p("laplace", 0, None, src, np.ones(2), tgt)
+
+
+def test_p2p_rows_match_per_row_dense():
+    rng = np.random.default_rng(5)
+    src = rng.normal(size=(80, 3))
+    w = rng.normal(size=80) + 1j * rng.normal(size=80)
+    tgt = rng.normal(size=(25, 3)) + 4
+    row_tgt = np.array([0, 3, 3, 11, 25])
+    row_ptr = np.array([0, 10, 30, 30, 77])
+    row_idx = rng.integers(0, 80, size=77).astype(np.int32)
+    out = oracle.p2p("helmholtz", 0, 2.5, src, w, tgt, rows=(row_tgt, row_ptr, row_idx))
+    for r in range(4):
+        sel = row_idx[row_ptr[r]:row_ptr[r + 1]]
+        ref = oracle.p2p("helmholtz", 0, 2.5, src[sel], w[sel], tgt[row_tgt[r]:row_tgt[r + 1]])
+        assert np.array_equal(out[row_tgt[r]:row_tgt[r + 1]], ref)
+
+
+def test_p2p_reference_core_agrees():
+    core = oracle.ref_core()
+    if core is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(9)
+    src = rng.normal(size=(120, 3))
+    tgt = rng.normal(size=(50, 3))
+    w = rng.normal(size=120) + 1j * rng.normal(size=120)
+    sn = rng.normal(size=(120, 3))
+    tn = rng.normal(size=(50, 3))
+    for v in range(3):
+        assert np.array_equal(oracle.p2p("laplace", v, None, src, w, tgt, sn, tn),
+                              core.laplace_p2p(v, src, w, sn, tgt, tn))
+        assert np.array_equal(oracle.p2p("helmholtz", v, 3.0, src, w, tgt, sn, tn),
+                              core.helmholtz_p2p(v, 3.0, src, w, sn, tgt, tn))
