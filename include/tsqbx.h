@@ -250,6 +250,25 @@ int tsqbx_p2p_helmholtz(int variant, double k, const double* src_xyz, const doub
                         int64_t ws_bytes, double* out, int64_t* err_key, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Box interaction lists -> row index lists: the gather of
+ * driver.direct_stage (driver.py:197-217, _gather_sources :109-113) for all
+ * target boxes at once.  Row r belongs to box row_box[r] (< 0: empty row); its
+ * sources are the owned source ranges [box_start[d*stride], box_end[d*stride])
+ * of the boxes d = lst_box[lst_ptr[b] .. lst_ptr[b+1]) concatenated in list
+ * order (pass owned_start[:, SOURCES] with stride 3 for the reference Octree).
+ * count: row_ptr (n_rows + 1) and *total (device scalar); fill: row_idx.
+ * ------------------------------------------------------------------------- */
+int64_t tsqbx_box_rows_workspace_bytes(int64_t n_rows);
+int tsqbx_box_rows_count(int64_t n_rows, const int64_t* row_box, const int64_t* lst_ptr,
+                         const int64_t* lst_box, const int64_t* box_start,
+                         const int64_t* box_end, int64_t box_stride, void* workspace,
+                         int64_t ws_bytes, int64_t* row_ptr, int64_t* total, void* stream);
+int tsqbx_box_rows_fill(int64_t n_rows, const int64_t* row_box, const int64_t* lst_ptr,
+                        const int64_t* lst_box, const int64_t* box_start, const int64_t* box_end,
+                        int64_t box_stride, const int64_t* row_ptr, int32_t* row_idx,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------
  * FP64 roofline probe: every thread runs 8 independent DFMA chains of `iters`
  * steps (16 * iters flops per thread); used by bench.py to measure the FP64
  * peak of the box (MEASURED_PEAKS.json has none).  out needs blocks*threads

@@ -31,6 +31,8 @@ def to_device(a, dtype: torch.dtype, dev: torch.device, shape=None) -> torch.Ten
         np_dtype = {torch.float64: np.float64, torch.int64: np.int64, torch.int32: np.int32,
                     torch.complex128: np.complex128}[dtype]
         arr = np.ascontiguousarray(np.asarray(a, dtype=np_dtype))
+        if not arr.flags.writeable:          # e.g. np.broadcast_to views
+            arr = arr.copy()
         t = torch.from_numpy(arr).to(device=dev, non_blocking=False)
     t = t.contiguous()
     if shape is not None:

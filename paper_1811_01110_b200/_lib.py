@@ -72,6 +72,9 @@ SIGNATURES = {
     "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_fp64_probe": (_I, [_P, _I64, _I, _I, _P]),
+    "tsqbx_box_rows_workspace_bytes": (_I64, [_I64]),
+    "tsqbx_box_rows_count": (_I, [_I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P]),
+    "tsqbx_box_rows_fill": (_I, [_I64, _P, _P, _P, _P, _P, _I64, _P, _P, _P]),
     "tsqbx_p2p_workspace_bytes": (_I64, [_I64, _I64, _I64, _I]),
     "tsqbx_p2p_packed": (_I, [_I, _I, _D, _P, _I64, _I, _I64, _P, _P, _P, _P, _P, _I64, _U, _P,
                               _I64, _P, _P, _P]),

@@ -155,7 +155,90 @@ def p2p_cases():
     return out
 
 
+def direct_stage_case():
+    """The driver's direct stages (driver.py:197-228) on the reference's own tree
+    and interaction lists (build_tree / compute_lists, the test_driver.py sphere
+    with TREE = TreeParams(nmax=40, t_f=0.9), plus 200 conventional targets):
+    the per-box loop is replayed with the compiled reference core, for three
+    kernels (Laplace S p=4, Laplace D p=6, Helmholtz S' k=1.3 p=5)."""
+    from gigaqbx import geometry as geo
+    from gigaqbx.ilists import compute_lists
+    from gigaqbx.tree import CENTERS, SOURCES, TARGETS, TreeParams, build_tree
+
+    disc = geo.make_sphere(1.0, 1, 6)
+    centers = geo.place_qbx_centers(disc, +1, 0.5)
+    rng = np.random.default_rng(17)
+    extra = rng.normal(size=(200, 3)) * 1.5
+    extra_n = rng.normal(size=(200, 3))
+    extra_n /= np.linalg.norm(extra_n, axis=1)[:, None]
+    tree = build_tree(disc.nodes, extra, centers.centers, centers.radii,
+                      TreeParams(nmax=40, t_f=0.9))
+    lists = compute_lists(tree, 20.0)
+    dens = rng.normal(size=disc.n_nodes) + 1j * rng.normal(size=disc.n_nodes)
+    w_src = disc.weights * dens
+    sperm = tree.perms[SOURCES]
+    w = np.empty_like(w_src)
+    w[...] = w_src[sperm]
+    sn = disc.normals[sperm]
+    tgt_of_center = centers.target_index[tree.perms[CENTERS]]
+    qtargets = disc.target_nodes[tgt_of_center]
+    qnormals = disc.target_normals[tgt_of_center]
+    conv = tree.points[TARGETS]
+    conv_n = extra_n[tree.perms[TARGETS]]
+    src = tree.points[SOURCES]
+    qc = tree.points[CENTERS]
+    out = dict(sources=src, weights=w, snormals=sn, conv=conv, conv_normals=conv_n,
+               qcenters=qc, qtargets=qtargets, qnormals=qnormals,
+               owned_start=tree.owned_start, owned_end=tree.owned_end,
+               target_boxes=lists.target_boxes)
+    kernels = [("lap_s", 0, 0, None, 4), ("lap_d", 0, 2, None, 6), ("helm_sp", 1, 1, 1.3, 5)]
+    for lname in ("list1", "list3close", "list4close"):
+        lst = getattr(lists, lname)
+        out[f"{lname}_starts"] = lst.starts
+        out[f"{lname}_flat"] = lst.flat
+        for kname, eq, var, k, p in kernels:
+            conv_near = np.zeros(conv.shape[0], complex)
+            qbx = np.zeros(qc.shape[0], complex)
+            n_ts = 0
+            for b in lists.target_boxes:                     # driver.py:199-227
+                b = int(b)
+                boxes = lst.get(b)
+                if boxes.shape[0] == 0:
+                    continue
+                sl = [tree.owned_slice(int(d), SOURCES) for d in boxes]
+                idx = np.concatenate([np.arange(x.start, x.stop) for x in sl])
+                if idx.shape[0] == 0:
+                    continue
+                ct = tree.owned_slice(b, TARGETS)
+                sn_b = np.ascontiguousarray(sn[idx]) if var == 2 else None
+                if ct.stop > ct.start:
+                    tn = np.ascontiguousarray(conv_n[ct]) if var == 1 else None
+                    if eq == 0:
+                        conv_near[ct] += core.laplace_p2p(var, src[idx], w[idx], sn_b,
+                                                          conv[ct], tn)
+                    else:
+                        conv_near[ct] += core.helmholtz_p2p(var, k, src[idx], w[idx], sn_b,
+                                                            conv[ct], tn)
+                cs = tree.owned_slice(b, CENTERS)
+                s_b = np.ascontiguousarray(src[idx])
+                w_b = np.ascontiguousarray(w[idx])
+                for ic in range(cs.start, cs.stop):
+                    tn_i = qnormals[ic] if var == 1 else None
+                    if eq == 0:
+                        qbx[ic] += core.ts_accum_laplace(var, p, s_b, w_b, sn_b, qc[ic],
+                                                         qtargets[ic], tn_i)
+                    else:
+                        qbx[ic] += core.ts_accum_helmholtz(var, k, p, s_b, w_b, sn_b, qc[ic],
+                                                           qtargets[ic], tn_i)
+                    n_ts += idx.shape[0]
+            out[f"{lname}_{kname}_conv"] = conv_near
+            out[f"{lname}_{kname}_qbx"] = qbx
+            out[f"{lname}_{kname}_nts"] = np.array(n_ts)
+    return out
+
+
 GOLDEN = {
+    "direct_stage": direct_stage_case,
     "pairs_p8": pair_cases,
     "backend_batch": backend_batch,
     "c1_literal": lambda: sphere_case(4096, 4, None, 3.0, False, 0),
