@@ -153,3 +153,121 @@ def pack_spheres(count: int, rng: np.random.Generator, box: float = 10.0, rmin: 
             origins.append(o)
             radii.append(R)
     return np.array(origins), np.array(radii)
+
+
+# ---------------------------------------------------------------------------
+# geometry files: the reference's JSON format
+# (geometry.py:432-498): arrays of numbers written as strings with 17
+# significant digits, optional centers block.
+# ---------------------------------------------------------------------------
+def _num_rows(a):
+    return [[format(float(x), ".17g") for x in row] for row in np.atleast_2d(a)]
+
+
+def _nums(a):
+    return [format(float(x), ".17g") for x in np.asarray(a).reshape(-1)]
+
+
+def save_geometry(path, disc: Discretization, centers: QbxCenterSet | None = None) -> None:
+    """Write ``disc`` (and ``centers``) in the reference's file format."""
+    import json
+
+    doc = {"nodes": _num_rows(disc.nodes), "weights": _nums(disc.weights),
+           "normals": _num_rows(disc.normals), "element_id": disc.element_id.tolist(),
+           "element_size": _nums(disc.element_size), "targets": _num_rows(disc.target_nodes),
+           "target_normals": _num_rows(disc.target_normals),
+           "target_element_id": disc.target_element_id.tolist()}
+    if centers is not None:
+        doc.update(centers=_num_rows(centers.centers), radii=_nums(centers.radii),
+                   target_index=centers.target_index.tolist(),
+                   side="exterior" if centers.side > 0 else "interior")
+    with open(path, "w") as f:
+        json.dump(doc, f)
+        f.write("\n")
+
+
+def load_geometry(path):
+    """(Discretization, QbxCenterSet | None) from a reference geometry file.
+    Missing target element ids / normals come from each target's nearest
+    quadrature node, as in the reference."""
+    import json
+
+    with open(path) as f:
+        doc = json.load(f)
+    f64 = lambda key: np.asarray(doc[key], dtype=np.float64)  # noqa: E731
+    nodes = f64("nodes").reshape(-1, 3)
+    targets = f64("targets").reshape(-1, 3)
+    element_id = np.asarray(doc["element_id"], dtype=np.int64)
+    normals = f64("normals").reshape(-1, 3)
+    nearest = None
+    if "target_element_id" not in doc or "target_normals" not in doc:
+        from scipy.spatial import cKDTree
+
+        nearest = cKDTree(nodes).query(targets)[1]
+    if "target_element_id" in doc:
+        teid = np.asarray(doc["target_element_id"], dtype=np.int64)
+    else:
+        teid = element_id[nearest]
+    if "target_normals" in doc:
+        tnrm = f64("target_normals").reshape(-1, 3)
+    else:
+        tnrm = normals[nearest]
+        tnrm = tnrm / np.linalg.norm(tnrm, axis=1)[:, None]
+    disc = Discretization(nodes=nodes, weights=f64("weights"), normals=normals,
+                          element_id=element_id, element_size=f64("element_size"),
+                          target_nodes=targets, target_normals=tnrm, target_element_id=teid)
+    centers = None
+    if "centers" in doc:
+        centers = QbxCenterSet(centers=f64("centers").reshape(-1, 3), radii=f64("radii"),
+                               target_index=np.asarray(doc["target_index"], dtype=np.int64),
+                               side=+1 if doc.get("side", "exterior") == "exterior" else -1)
+    return disc, centers
+
+
+@dataclass
+class DeviceGeometry:
+    """A geometry resident in HBM, laid out for the TSQBX path: sources with
+    their quadrature weights and normals, centers with radii, and each center's
+    on-surface target (and its normal) -- one target per center."""
+
+    nodes: "object"
+    weights: "object"
+    normals: "object"
+    centers: "object"
+    radii: "object"
+    targets: "object"
+    target_normals: "object"
+
+    @classmethod
+    def from_host(cls, disc: Discretization, centers: QbxCenterSet, device=None):
+        import torch
+
+        from . import _device as dv
+
+        dev = dv.require_cuda(device)
+        put = lambda a: dv.to_device(a, torch.float64, dev)  # noqa: E731
+        return cls(nodes=put(disc.nodes), weights=put(disc.weights), normals=put(disc.normals),
+                   centers=put(centers.centers), radii=put(centers.radii),
+                   targets=put(disc.target_nodes[centers.target_index]),
+                   target_normals=put(disc.target_normals[centers.target_index]))
+
+    def near_field(self, cfg, density, near_mult: float = 3.0, validate: bool = True):
+        """Per-center near-field TSQBX potentials of ``density`` (one value per
+        node; source weights = quadrature weight x density): near lists are
+        the radius balls |s - c| <= near_mult * r_c (BASELINE's definition),
+        built and evaluated on the device.  Returns a complex128 CUDA tensor
+        (the center's target order)."""
+        import torch
+
+        from . import _device as dv
+        from .tsqbx import near_field_potentials
+
+        dens = dv.to_device(density, torch.complex128, self.nodes.device, (-1,))
+        if dens.shape[0] != self.nodes.shape[0]:
+            raise ValueError("density must have one value per source node")
+        w = self.weights.to(torch.complex128) * dens
+        nrm = self.normals if cfg.spec.needs_source_normals else None
+        tn = self.target_normals if cfg.spec.needs_target_normals else None
+        return near_field_potentials(cfg, self.nodes, w, self.centers, self.radii * near_mult,
+                                     self.targets, source_normals=nrm, target_normals=tn,
+                                     validate=validate)

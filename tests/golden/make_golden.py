@@ -237,7 +237,37 @@ def direct_stage_case():
     return out
 
 
+def geometry_case():
+    """Geometry files written by the reference (geometry.save_geometry,
+    geometry.py:436-455): a sphere with centers, and the same file without the
+    optional target_element_id / target_normals / centers keys (load_geometry
+    then recovers them by nearest node, :464-476).  The npz holds what the
+    reference's load_geometry returns for the minimal file."""
+    import json
+
+    from gigaqbx import geometry as geo
+
+    disc = geo.make_sphere(1.0, 0, 3)
+    centers = geo.place_qbx_centers(disc, -1, 0.5)
+    full = os.path.join(HERE, "geom_sphere.json")
+    geo.save_geometry(full, disc, centers)
+    with open(full) as f:
+        doc = json.load(f)
+    for key in ("target_element_id", "target_normals", "centers", "radii", "target_index",
+                "side"):
+        doc.pop(key)
+    minimal = os.path.join(HERE, "geom_sphere_min.json")
+    with open(minimal, "w") as f:
+        json.dump(doc, f)
+        f.write("\n")
+    d2, c2 = geo.load_geometry(minimal)
+    assert c2 is None
+    return dict(target_element_id=d2.target_element_id, target_normals=d2.target_normals,
+                nodes=disc.nodes, centers=centers.centers, radii=centers.radii)
+
+
 GOLDEN = {
+    "geometry": geometry_case,
     "direct_stage": direct_stage_case,
     "pairs_p8": pair_cases,
     "backend_batch": backend_batch,

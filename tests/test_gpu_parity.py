@@ -242,6 +242,14 @@ def _case_parity(case, tol, subset=None, generic=False):
     return out, near
 
 
+@pytest.mark.parametrize("name,preset", [("c4", "literal"), ("c4", "dense"), ("c5", "literal")])
+def test_c4_c5_full_size_one_percent(name, preset):
+    # parity on a >= 1% seeded subset at the full C4/C5 sizes
+    case = configs.make_case(name, preset)
+    _case_parity(case, LAP_TOL if name == "c4" else HELM_TOL,
+                 subset=max(4096, case.n_centers // 100))
+
+
 @pytest.mark.parametrize("name,preset", [("c1", "literal"), ("c1", "dense")])
 def test_c1_full(name, preset):
     _case_parity(configs.make_case(name, preset), LAP_TOL)
