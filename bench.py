@@ -357,6 +357,37 @@ def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
     return res, prob, clocks
 
 
+P2P_FLOPS = {(0, 0): 13, (0, 1): 21, (0, 2): 21, (1, 0): 23, (1, 1): 35, (1, 2): 35}
+
+
+def measure_p2p(torch, dev, flush, peak, n=65536, reps=5):
+    """dense direct sums (kernels.direct_sum's kernel) over
+    n x n pairs, sources and targets resident; algorithmic flops per pair
+    (DESIGN.md): Laplace 13 (S) / 21 (S', D), Helmholtz 23 / 35."""
+    from paper_1811_01110_b200 import KernelSpec, P2PProblem
+    from paper_1811_01110_b200.kernels import Equation, Variant
+    rng = np.random.default_rng(0)
+    src = torch.as_tensor(rng.normal(size=(n, 3)), device=dev)
+    tgt = torch.as_tensor(rng.normal(size=(n, 3)) + 0.01, device=dev)
+    w = torch.as_tensor(rng.normal(size=n) + 1j * rng.normal(size=n), device=dev)
+    res = {}
+    for eq, k in ((Equation.LAPLACE, None), (Equation.HELMHOLTZ, 10.0)):
+        spec = KernelSpec(equation=eq, variant=Variant.SINGLE_LAYER, helmholtz_k=k)
+        prob = P2PProblem(spec, src, w, device=dev)
+        out = torch.empty(n, dtype=torch.complex128, device=dev)
+        step = lambda: prob.evaluate(tgt, validate=False, out=out)  # noqa: E731
+        for _ in range(2):
+            step()
+        ms = time_device_steps(torch, step, reps, flush)
+        mean = sum(ms) / len(ms)
+        rate = n * n / (mean * 1e-3)
+        fpp = P2P_FLOPS[(0 if eq is Equation.LAPLACE else 1, 0)]
+        res[f"{eq.value}_s_{n}x{n}"] = {
+            "value": rate, "unit": "pair-evals/s", "ms_per_step": mean, "flops_per_pair": fpp,
+            "roofline_frac": rate * fpp / (peak * 1e12) if peak else None}
+    return res
+
+
 def measure_e2e(torch, case, args, dev, with_near_lists=False):
     """Through the public API with host (pinned) buffers, every step: H2D of the
     step's inputs, TSQBX (validated), D2H of the potentials into a pinned buffer.
@@ -479,7 +510,8 @@ def main_ours(args):
         sec = {}
         del prob
         for name, preset in (("c2", "literal" if case.preset == "dense" else "dense"),
-                             ("c3", "dense"), ("c3", "literal")):
+                             ("c3", "dense"), ("c3", "literal"), ("c4", "literal"),
+                             ("c4", "dense"), ("c5", "literal"), ("c5", "dense")):
             if name == case.name and preset == case.preset:
                 continue
             c2 = configs.make_case(name, preset)
@@ -493,6 +525,7 @@ def main_ours(args):
             del p2
             torch.cuda.empty_cache()
         line["secondary"] = sec
+        line["p2p"] = measure_p2p(torch, dev, flush, peak)
     print(json.dumps(line))
     return 0
 
