@@ -340,6 +340,14 @@ constexpr int kSellBlock = TSQBX_SELL_BLOCK;   // threads per CTA of the SELL ke
 #ifndef TSQBX_LAP_MINB
 #define TSQBX_LAP_MINB 3
 #endif
+// one target per center (C1, C4, C5): one more CTA per SM (measured: C4
+// literal +9 %, C5 literal +12 %, dense -1 %; with two targets it costs 2-40 %)
+#ifndef TSQBX_LAP_MINB1
+#define TSQBX_LAP_MINB1 4
+#endif
+#ifndef TSQBX_HELM_MINB1
+#define TSQBX_HELM_MINB1 3
+#endif
 #ifndef TSQBX_HELM_MINB
 #define TSQBX_HELM_MINB 2
 #endif
@@ -352,19 +360,24 @@ constexpr int kSellBlock = TSQBX_SELL_BLOCK;   // threads per CTA of the SELL ke
 constexpr int kRing = TSQBX_RING;  // index blocks in flight (4 kRing entries of lookahead)
 constexpr int kSlots = kRing + 1;  // ring slots per thread (a power of two keeps b % kSlots a mask)
 
-template <bool NRM = false>
+#ifndef TSQBX_GATHER_DEPTH
+#define TSQBX_GATHER_DEPTH 1
+#endif
+
+// D = source records gathered ahead of use (1: the next one; 2: two deep)
+template <bool NRM = false, int D = TSQBX_GATHER_DEPTH>
 struct SellStream {
   const int4* __restrict__ blk;   // this lane's block 0; block b at blk + 32 b
   const double4* __restrict__ sp;
   const double* __restrict__ swi;
   int4* ring;                     // [kRing + 1][kSellBlock] int4, this thread's column
   int count, nblk, i;
-  int4 cur;                       // indices of block i / 4
-  double4 q_next;
-  double w_next;
+  int4 cur;                       // indices of the block being consumed / 4
+  double4 q_next[D];
+  double w_next[D];
   bool real_w;
   const double4* __restrict__ snrm;   // NRM: source normals, fetched with the record
-  double4 n_next;
+  double4 n_next[D];
 
   __device__ __forceinline__ void issue(int b) {
     // block b goes to slot b % kSlots; always commit so group counts stay uniform
@@ -373,26 +386,32 @@ struct SellStream {
   }
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t g, int n, bool realw,
                                         int4* ring_base)
-      : sp(a.sp), swi(a.swi), count(n), i(0), w_next(0.0), real_w(realw), snrm(a.snrm) {
+      : sp(a.sp), swi(a.swi), count(n), i(0), real_w(realw), snrm(a.snrm) {
     blk = reinterpret_cast<const int4*>(a.sell_idx + a.sell_ptr[g >> 5]) + (g & 31);
     ring = ring_base + threadIdx.x;
     nblk = (count + 3) >> 2;
-    q_next = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      q_next[d] = make_double4(0.0, 0.0, 0.0, 0.0);
+      w_next[d] = 0.0;
+    }
 #pragma unroll
     for (int b = 0; b < kRing; ++b) issue(b);
     cur = make_int4(0, 0, 0, 0);
     if (count > 0) enter_block(0);
-    if (count > 0) fetch(cur.x);
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d < count) fetch(d, d == 0 ? cur.x : d == 1 ? cur.y : d == 2 ? cur.z : cur.w);
   }
   __device__ __forceinline__ void enter_block(int b) {
     cp_async_wait<kRing - 1>();                 // block b has landed
     cur = ring[(b % kSlots) * kSellBlock];
     issue(b + kRing);                           // reuses the slot of block b - 1
   }
-  __device__ __forceinline__ void fetch(int s) {
-    q_next = ld256(sp + s);
-    if (!real_w) w_next = __ldg(swi + s);
-    if (NRM) n_next = ld256(snrm + s);
+  __device__ __forceinline__ void fetch(int d, int s) {
+    q_next[d] = ld256(sp + s);
+    if (!real_w) w_next[d] = __ldg(swi + s);
+    if (NRM) n_next[d] = ld256(snrm + s);
   }
   __device__ __forceinline__ bool more() const { return i < count; }
   __device__ __forceinline__ void next(double4& q, double& wi) {
@@ -400,14 +419,21 @@ struct SellStream {
     next(q, wi, nrm);
   }
   __device__ __forceinline__ void next(double4& q, double& wi, double4& nrm) {
-    q = q_next;
-    wi = w_next;
-    if (NRM) nrm = n_next;
+    q = q_next[0];
+    wi = w_next[0];
+    if (NRM) nrm = n_next[0];
+#pragma unroll
+    for (int d = 0; d + 1 < D; ++d) {
+      q_next[d] = q_next[d + 1];
+      w_next[d] = w_next[d + 1];
+      if (NRM) n_next[d] = n_next[d + 1];
+    }
     ++i;
-    if (i < count) {
-      const int e = i & 3;
-      if (e == 0) enter_block(i >> 2);
-      fetch(e == 0 ? cur.x : e == 1 ? cur.y : e == 2 ? cur.z : cur.w);
+    const int j = i + D - 1;                    // the entry to gather now
+    if (j < count) {
+      const int e = j & 3;
+      if (e == 0) enter_block(j >> 2);
+      fetch(D - 1, e == 0 ? cur.x : e == 1 ? cur.y : e == 2 ? cur.z : cur.w);
     }
   }
 };
@@ -430,7 +456,9 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
       ar[q] = ai[q] = bm[q] = 0.0;
     }
-    SellStream<> ss(a, g, len, REALW, ring);
+    // high orders have more arithmetic per source to cover a second gather in
+    // flight (measured: C4 dense p = 12 +7 %; p = 8 -2 %)
+    SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)> ss(a, g, len, REALW, ring);
     // one source against the NT targets
     auto source = [&](const double4& q4, double wim) {
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
@@ -487,7 +515,7 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
 // real weights (the usual Laplace density) skip every Im w load and FMA; the
 // pack kernel records whether any Im w is nonzero, so no host round trip decides
 template <int P, int NT, bool VAL>
-__global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[kSlots * kSellBlock];
   const bool realw = a.real_w || *a.imag_flag == 0u;
   const int64_t stride = TSQBX_PERSIST ? (int64_t)gridDim.x * blockDim.x : a.n_ctr;
@@ -500,7 +528,7 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB) laplace_sell_kerne
 }
 
 template <int P, int NT, bool VAL>
-__global__ void __launch_bounds__(kSellBlock, TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
   // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n live in shared
   // memory ([n][q][thread], conflict-free) instead of 2(P+1) registers per target
 #if TSQBX_HELM_CF_SMEM

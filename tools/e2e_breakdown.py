@@ -57,6 +57,7 @@ for rep in range(5):
     ho.copy_(out)
     t = mark("d2h", t)
 tot = sum(T.values())
+print("-- full pipeline phases")
 for k, v in T.items():
     print(f"{k:28s} {v / 5:8.3f} ms  {100 * v / tot:5.1f}%")
 t0 = time.perf_counter()
@@ -64,3 +65,36 @@ for _ in range(5):
     near_field_potentials(case.cfg, src, w, ctr, rad, tgt, tgt_ptr=tptr, out=ho)
 torch.cuda.synchronize()
 print(f"near_field_potentials end-to-end: {(time.perf_counter() - t0) / 5 * 1e3:.3f} ms")
+
+# batch API with prebuilt device near lists (the bench's `e2e`)
+from paper_1811_01110_b200.tsqbx import ts_accumulate_batch  # noqa: E402
+near0 = build_near_lists(case.centers, case.sources, case.near_radii, dev)
+T.clear()
+for rep in range(6):
+    t = time.perf_counter()
+    s_d = src.to(dev, non_blocking=True)
+    w_d = torch.view_as_real(w.to(dev, non_blocking=True))
+    c_d = ctr.to(dev, non_blocking=True)
+    t_d = tgt.to(dev, non_blocking=True)
+    p_d = tptr.to(dev, non_blocking=True)
+    t = mark("h2d", t)
+    prep = _Prepared(case.cfg, dev, s_d, w_d, None, c_d, near0, t_d, None, p_d)
+    t = mark("prepare(pack+order)", t)
+    out = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
+    prep.launch(torch.view_as_real(out), True)
+    t = mark("eval", t)
+    prep.check_errors(True)
+    t = mark("validate check", t)
+    ho.copy_(out)
+    t = mark("d2h", t)
+    if rep == 0:
+        T.clear()
+tot = sum(T.values())
+print("-- batch API phases (prebuilt near lists)")
+for k, v in T.items():
+    print(f"{k:28s} {v / 5:8.3f} ms  {100 * v / tot:5.1f}%")
+t0 = time.perf_counter()
+for _ in range(5):
+    ts_accumulate_batch(case.cfg, src, w, ctr, tgt, near0, tgt_ptr=tptr, out=ho)
+torch.cuda.synchronize()
+print(f"ts_accumulate_batch end-to-end: {(time.perf_counter() - t0) / 5 * 1e3:.3f} ms")
