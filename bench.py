@@ -62,6 +62,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--group-lanes", type=int, default=0)
+    ap.add_argument("--force-dist", action="store_true",
+                    help=argparse.SUPPRESS)   # run the N>1 code path at world size 1 (tests)
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="N>1: independent problem per GPU (weak) or one sharded problem")
     return ap.parse_args()
 
 
@@ -445,7 +449,7 @@ def main_ours(args):
     dev = torch.device("cuda", local)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     case = configs.make_case(args.case, args.preset)
-    if world > 1:
+    if world > 1 or args.force_dist:
         return main_distributed(torch, args, case, dev, flush, rank, world, local)
 
     peak = fp64_peak_tflops(torch, dev)
@@ -531,46 +535,84 @@ def main_ours(args):
 
 
 def main_distributed(torch, args, case, dev, flush, rank, world, local):
+    """N ranks, one GPU each.  Default (`--scaling weak`, the tier rule for a
+    path that partitions): every rank owns an independent problem of the N=1
+    size (same configuration, seed = rank) and evaluates it with no data-path
+    collective; the step time is the max over ranks (device events, all-reduced
+    after the timed region) and `value` = all ranks' pairs / that time.
+    `--scaling strong`: one problem split by pair count over the ranks plus one
+    NCCL all-gather of the potentials per step (`ShardedEvaluator`)."""
     import torch.distributed as dist
     from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs
     from paper_1811_01110_b200.distributed import ShardedEvaluator
 
     dist.init_process_group("nccl", device_id=dev)
+    weak = args.scaling == "weak"
+    if weak:
+        case = configs.make_case(args.case, args.preset, seed=rank)
     near = build_near_lists(case.centers, case.sources, case.near_radii, dev)
     prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
                         tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev)
     pairs = prob.pair_count()
-    sh = ShardedEvaluator(prob, rank, world)
+    step = prob.evaluate if weak else ShardedEvaluator(prob, rank, world).evaluate
     for _ in range(max(3, args.warmup)):
-        sh.evaluate()
+        step()
     torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    ms = time_device_steps(torch, sh.evaluate, args.steps, flush)
-    torch.cuda.synchronize()
-    dist.barrier()
-    total = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
-    dist.all_reduce(total, op=dist.ReduceOp.MAX)
-    t = float(total.item())
+    sampler = ClockSampler(local)
+    with sampler:
+        t_end = time.perf_counter() + args.soak_seconds
+        while time.perf_counter() < t_end:     # soak: clocks settle under this load
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms = time_device_steps(torch, step, args.steps, flush)
+        torch.cuda.synchronize()
+        dist.barrier()
+    clocks = sampler.summary()
+    stats = torch.tensor([sum(ms), float(pairs)], dtype=torch.float64, device=dev)
+    tmax = stats[:1].clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tot_pairs = stats[1:].clone()
+    dist.all_reduce(tot_pairs, op=dist.ReduceOp.SUM)
+    e2e = None
+    if weak and not args.no_e2e:
+        r = measure_e2e(torch, case, args, dev)
+        e_ms = torch.tensor([sum(r["ms"]) / len(r["ms"])], dtype=torch.float64, device=dev)
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(tot_pairs.item()) / (float(e_ms.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": r["h2d"] * world, "d2h_bytes_per_step": r["d2h"] * world,
+               "ms_per_step": float(e_ms.item()),
+               "path": "ts_accumulate_batch on every rank (pinned host in/out), max over ranks"}
+    t = float(tmax.item())
+    step_pairs = float(tot_pairs.item()) if weak else float(pairs)
     if rank == 0:
         fpp = configs.algorithmic_flops_per_pair(case.cfg.spec, case.cfg.p_qbx)
-        line = {"metric": METRIC, "value": pairs * args.steps / (t * 1e-3), "unit": UNIT,
+        per_gpu_tf = step_pairs * fpp / (t / args.steps * 1e-3) / 1e12 / world
+        peak = fp64_peak_tflops(torch, dev)
+        line = {"metric": METRIC, "value": step_pairs * args.steps / (t * 1e-3), "unit": UNIT,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": t / args.steps, "higher_is_better": True, "scaling": "strong",
+                "ms_per_step": t / args.steps, "higher_is_better": True,
+                "scaling": "weak" if weak else "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_name(case), "case": case.name,
-                           "preset": case.preset, "pairs_per_step": pairs,
-                           "parallelism": f"centers sharded by pair count over {world} ranks, "
-                                          "sources replicated, 1 NCCL all-gather per step"},
-                "roofline": {"bound": "fp64", "achieved": pairs * fpp / (t / args.steps * 1e-3)
-                             / 1e12 / world, "unit": "TFLOP/s per GPU", "peak": None,
-                             "frac": None, "traffic": None},
-                "gpu_launches": 2 * args.steps}
+                           "preset": case.preset, "pairs_per_step": step_pairs,
+                           "l2": "flushed between steps (256 MB write, outside the timed events)",
+                           "parallelism": (f"{world} independent problems (seed = rank), one per "
+                                           "GPU, no data-path collective" if weak else
+                                           f"centers sharded by pair count over {world} ranks, "
+                                           "sources replicated, 1 NCCL all-gather per step")},
+                "roofline": {"bound": "fp64", "achieved": per_gpu_tf, "unit": "TFLOP/s per GPU",
+                             "peak": peak, "frac": per_gpu_tf / peak if peak else None,
+                             "traffic": None},
+                "gpu_launches": (1 if weak else 2) * args.steps,
+                "clocks": clocks}
+        if e2e:
+            line["e2e"] = e2e
         print(json.dumps(line))
     dist.destroy_process_group()
     return 0
-
-
 def main():
     args = parse_args()
     if args.impl == "reference":
