@@ -386,22 +386,38 @@ struct SellStream {
   }
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t g, int n, bool realw,
                                         int4* ring_base)
+      : SellStream(a, a.sell_ptr[g >> 5], g, n, realw, ring_base, true) {}
+  // `soff` = sell_ptr[g / 32], loaded by the caller; go = false only issues the
+  // first kRing index blocks (start() later waits for block 0 and gathers)
+  __device__ __forceinline__ SellStream(const EvalParams& a, int64_t soff, int64_t g, int n,
+                                        bool realw, int4* ring_base, bool go)
       : sp(a.sp), swi(a.swi), count(n), i(0), real_w(realw), snrm(a.snrm) {
-    blk = reinterpret_cast<const int4*>(a.sell_idx + a.sell_ptr[g >> 5]) + (g & 31);
+    blk = reinterpret_cast<const int4*>(a.sell_idx + soff) + (g & 31);
     ring = ring_base + threadIdx.x;
     nblk = (count + 3) >> 2;
+    issue_first();
+    if (go) start();
+  }
+  __device__ __forceinline__ void issue_first() {
+#pragma unroll
+    for (int b = 0; b < kRing; ++b) issue(b);
+  }
+  __device__ __forceinline__ void start() {
+    i = 0;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       q_next[d] = make_double4(0.0, 0.0, 0.0, 0.0);
       w_next[d] = 0.0;
     }
-#pragma unroll
-    for (int b = 0; b < kRing; ++b) issue(b);
     cur = make_int4(0, 0, 0, 0);
     if (count > 0) enter_block(0);
 #pragma unroll
     for (int d = 0; d < D; ++d)
       if (d < count) fetch(d, d == 0 ? cur.x : d == 1 ? cur.y : d == 2 ? cur.z : cur.w);
+  }
+  __device__ __forceinline__ void restart() {
+    issue_first();
+    start();
   }
   __device__ __forceinline__ void enter_block(int b) {
     cp_async_wait<kRing - 1>();                 // block b has landed
@@ -438,11 +454,37 @@ struct SellStream {
   }
 };
 
+// Row metadata every SELL kernel needs first.  Loaded before anything that
+// depends on a load (the real-weight flag, the target range), so the four
+// independent first-level loads overlap instead of forming a chain.
+struct RowHead {
+  int64_t soff, t0, t1;
+  double cx, cy, cz;
+  int len;
+};
+__device__ __forceinline__ RowHead load_head(const EvalParams& a, int64_t g) {
+  RowHead h;
+  h.soff = a.sell_ptr[g >> 5];
+  h.len = (int)(a.nptr[g + 1] - a.nptr[g]);
+  h.t0 = a.tptr[g];
+  h.t1 = a.tptr[g + 1];
+  h.cx = a.ctr[3 * g];
+  h.cy = a.ctr[3 * g + 1];
+  h.cz = a.ctr[3 * g + 2];
+  return h;
+}
+
 template <int P, int NT, bool VAL, bool REALW>
-__device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g, int4* ring) {
-  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
-  const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+__device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g,
+                                                  const RowHead& h, int4* ring) {
+  const double cx = h.cx, cy = h.cy, cz = h.cz;
+  const int len = h.len;
+  const int64_t t0 = h.t0, t1 = h.t1;
+  // high orders have more arithmetic per source to cover a second gather in
+  // flight (measured: C4 dense p = 12 +7 %; p = 8 -2 %)
+  using Stream = SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)>;
+  // the index ring starts filling before the target range is known
+  Stream ss(a, h.soff, g, len, REALW, ring, false);
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
     int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
@@ -456,9 +498,8 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
       ar[q] = ai[q] = bm[q] = 0.0;
     }
-    // high orders have more arithmetic per source to cover a second gather in
-    // flight (measured: C4 dense p = 12 +7 %; p = 8 -2 %)
-    SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)> ss(a, g, len, REALW, ring);
+    if (tb == t0) ss.start();
+    else ss.restart();
     // one source against the NT targets
     auto source = [&](const double4& q4, double wim) {
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
@@ -510,6 +551,7 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       }
     }
   }
+  if (t0 >= t1) cp_async_wait<0>();   // no pass consumed the ring: drain it before exit
 }
 
 // real weights (the usual Laplace density) skip every Im w load and FMA; the
@@ -517,13 +559,14 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
 template <int P, int NT, bool VAL>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[kSlots * kSellBlock];
-  const bool realw = a.real_w || *a.imag_flag == 0u;
   const int64_t stride = TSQBX_PERSIST ? (int64_t)gridDim.x * blockDim.x : a.n_ctr;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ctr; g += stride) {
+    const RowHead h = load_head(a, g);
+    const bool realw = a.real_w || *a.imag_flag == 0u;
     if (realw)
-      laplace_sell_body<P, NT, VAL, true>(a, g, ring);
+      laplace_sell_body<P, NT, VAL, true>(a, g, h, ring);
     else
-      laplace_sell_body<P, NT, VAL, false>(a, g, ring);
+      laplace_sell_body<P, NT, VAL, false>(a, g, h, ring);
   }
 }
 

@@ -404,3 +404,35 @@ def test_derivative_variants_all_orders(p, eq):
         ref = oracle.ts_batch(eq, spec.variant_code, spec.helmholtz_k or 0.0, p, src, w, ctr,
                               nptr, nidx, tgt, tptr, snormals=sn, tnormals=tn)
         assert normwise(out, ref) <= (LAP_TOL if eq == "laplace" else HELM_TOL), (variant, p)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("band", [(0.05, 0.7), (0.5, 1.5), (1.2, 1.6), (0.5, 6.0)])
+def test_helmholtz_sin_cos_ranges(variant, band):
+    """kR inside pi/4 (narrow series), straddling it (wide series), near pi/2,
+    and beyond (library sincos) -- mixed within warps -- against the oracle."""
+    rng = np.random.default_rng(int(band[1] * 10))
+    k = 20.0
+    n_ctr, per = 96, 24
+    ctr = rng.normal(size=(n_ctr, 3))
+    dirs = rng.normal(size=(n_ctr * per, 3))
+    dirs /= np.linalg.norm(dirs, axis=1)[:, None]
+    R = rng.uniform(band[0], band[1], size=n_ctr * per) / k
+    src = np.repeat(ctr, per, axis=0) + dirs * R[:, None]
+    sn = rng.normal(size=src.shape)
+    sn /= np.linalg.norm(sn, axis=1)[:, None]
+    w = rng.normal(size=src.shape[0]) + 1j * rng.normal(size=src.shape[0])
+    nptr = np.arange(0, n_ctr * per + 1, per)
+    nidx = np.arange(n_ctr * per, dtype=np.int32)
+    tdir = rng.normal(size=(n_ctr, 3))
+    tdir /= np.linalg.norm(tdir, axis=1)[:, None]
+    tgt = ctr + tdir * (0.4 * band[0] / k)
+    tn = rng.normal(size=(n_ctr, 3))
+    tn /= np.linalg.norm(tn, axis=1)[:, None]
+    spec = KernelSpec(equation=Equation.HELMHOLTZ, variant=variant, helmholtz_k=k)
+    cfg = TsConfig(spec, 10)
+    out = ts_accumulate_batch(cfg, src, w, ctr, tgt, (nptr, nidx), source_normals=sn,
+                              target_normals=tn)
+    ref = oracle.ts_batch("helmholtz", spec.variant_code, k, 10, src, w, ctr, nptr, nidx, tgt,
+                          np.arange(n_ctr + 1, dtype=np.int64), snormals=sn, tnormals=tn)
+    assert normwise(out, ref) <= HELM_TOL
