@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 4
+#define TSQBX_ABI_VERSION 5
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -207,6 +207,27 @@ int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* se
  * all-gathered shards into user target order. */
 int tsqbx_scatter_c128(int64_t n, const int64_t* dest, const double* src, double* out,
                        void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Single call: one (center, target) over a source batch -- the reference's
+ * per-call protocol (_core.ts_accum_laplace / ts_accum_helmholtz,
+ * _core.pyx:205-207, :310-312, and tsqbx.ts_accumulate, tsqbx.py:68-80): one
+ * launch and a stream synchronisation; small batches (<= 256 KB staged) are
+ * read from / written to the pinned host buffers in place, larger ones take one
+ * H2D and one D2H copy through device_buf.
+ * staged_host (pinned) holds tsqbx_one_staging_doubles(n, variant == D) doubles:
+ *   [center(3) target(3) target_normal(3) |t-c| 0 x 6]   (|t-c| as the caller's
+ *                                                       validation computed it)
+ *   [x y z Re(w)] x n  [Im(w)] x n  [0 pad to a multiple of 4]  ([nx ny nz 0] x n for D)
+ * device_buf holds at least that + 4 doubles.  result_host (pinned) receives
+ * {Re, Im, err_key}: the reference's value and, with TSQBX_FLAG_VALIDATE, the
+ * exact _prep key ((kind << 31) | position, kind 0 = coincident, 1 =
+ * separation; TSQBX_ERR_KEY_NONE when valid), stored as int64 bits.
+ * ------------------------------------------------------------------------- */
+int64_t tsqbx_one_staging_doubles(int64_t n_src, int with_normals);
+int tsqbx_eval_one(int equation, int variant, double k, int p, const double* staged_host,
+                   int64_t n_src, unsigned flags, double* device_buf, int64_t device_doubles,
+                   double* result_host, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Point-to-point direct interactions: replaces the

@@ -4,18 +4,16 @@ Same signatures and conventions as ``_core.ts_accum_laplace`` /
 ``_core.ts_accum_helmholtz`` (_core.pyx:205-207, :310-312; _ref.py:177, :278):
 one (center, target) over a source batch, no validation (backends never
 validate; tsqbx._prep does), empty batch -> 0j, Laplace with real weights has
-an exactly-zero imaginary part.  Each call is a batch-of-one launch of the
-same kernels ``ts_accumulate_batch`` uses.
+an exactly-zero imaginary part.  Each call is one H2D copy, one launch of the
+single-call kernel and one D2H copy (``_single.py``); batches belong in
+``ts_accumulate_batch``.
 """
 
 from __future__ import annotations
 
 import numpy as np
-import torch
 
-from .. import _device as dv
 from ..kernels import Equation, KernelSpec, Variant
-from ..nearlist import NearLists
 
 BACKEND_NAME = "cuda"
 
@@ -24,27 +22,21 @@ _VARIANTS = {0: Variant.SINGLE_LAYER, 1: Variant.TARGET_NORMAL_DERIV,
 
 
 def _one(spec: KernelSpec, p, sources, weights, snormals, center, target, tnormal) -> complex:
-    from ..tsqbx import TsConfig, _Prepared, _inputs
+    from .._single import one_call
+    from ..tsqbx import _equation_code
 
     sources = np.ascontiguousarray(sources, dtype=np.float64).reshape(-1, 3)
-    n = sources.shape[0]
-    if n == 0:
+    if sources.shape[0] == 0:
         return 0.0 + 0.0j
-    cfg = TsConfig(spec, int(p))
-    dev = dv.require_cuda()
-    tn = None if tnormal is None else np.asarray(tnormal, dtype=np.float64).reshape(1, 3)
-    src, w, ctr, tgt, sn, tnd = _inputs(cfg, sources, weights,
-                                        np.asarray(center, dtype=np.float64).reshape(1, 3),
-                                        np.asarray(target, dtype=np.float64).reshape(1, 3),
-                                        snormals, tn, dev)
-    near = NearLists(n_ctr=1, n_src=n, n_pairs=n,
-                     ptr=torch.tensor([0, n], dtype=torch.int64, device=dev),
-                     csr_idx=torch.arange(n, dtype=torch.int32, device=dev))
-    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tnd,
-                     torch.tensor([0, 1], dtype=torch.int64, device=dev))
-    out = torch.empty(1, dtype=torch.complex128, device=dev)
-    prep.launch(torch.view_as_real(out), validate=False)
-    return complex(out.cpu().numpy()[0])
+    weights = np.ascontiguousarray(weights, dtype=np.complex128).reshape(-1)
+    sn = (np.ascontiguousarray(snormals, dtype=np.float64).reshape(-1, 3)
+          if spec.needs_source_normals else None)
+    tn = (np.asarray(tnormal, dtype=np.float64).reshape(3)
+          if spec.needs_target_normals else None)
+    value, _ = one_call(_equation_code(spec), spec.variant_code, float(spec.helmholtz_k or 0.0),
+                        int(p), sources, weights, sn, np.asarray(center, np.float64).reshape(3),
+                        np.asarray(target, np.float64).reshape(3), tn, validate=False)
+    return value
 
 
 def ts_accum_laplace(variant, p, sources, weights, snormals, center, target, tnormal):

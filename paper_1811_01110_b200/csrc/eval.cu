@@ -1005,9 +1005,160 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
 }
 
 // ---------------------------------------------------------------------------
-// Generic kernel: runtime order, every variant, reference operation order
-// (_core.pyx:229-306 and :365-418).  One target per pass.
+// Generic per-pair arithmetic: runtime order, every variant, reference
+// operation order (_core.pyx:229-306 and :365-418).  Shared by the generic
+// batch kernel and the single-call kernel.
 // ---------------------------------------------------------------------------
+struct GenericTarget {
+  double c[3];      // center
+  double r;         // |t - c|
+  double th[3];     // (t - c)/r, 0 at r = 0
+  double nt[3];     // target normal (S')
+  const double* jt;   // Helmholtz: j_n(k r), n <= p
+  const double* jtp;  // Helmholtz: j'_n(k r)
+};
+
+// (sre, sim) = the kernel sum of one source (before the weight and the
+// 1/(4 pi) or ik/(4 pi) factor); rho = r / R for the separation screen
+__device__ __forceinline__ void generic_pair(int equation, int variant, int p, double k,
+                                             const GenericTarget& T, const double4& q4,
+                                             const double4* n4p, double& sre, double& sim,
+                                             double& rho_out) {
+  const double* c = T.c;
+  const double r = T.r;
+  const double* th = T.th;
+  const double* nt = T.nt;
+  const double* jt = T.jt;
+  const double* jtp = T.jtp;
+  const double sc[3] = {q4.x - c[0], q4.y - c[1], q4.z - c[2]};
+  const double R = sqrt(sc[0] * sc[0] + sc[1] * sc[1] + sc[2] * sc[2]);
+  const double sh[3] = {sc[0] / R, sc[1] / R, sc[2] / R};
+  double cg = 1.0;
+  if (r > 0.0) cg = fmin(1.0, fmax(-1.0, sh[0] * th[0] + sh[1] * th[1] + sh[2] * th[2]));
+  const double rho = r / R;
+  rho_out = rho;
+  double ns[3] = {0.0, 0.0, 0.0};
+  if (variant == 2) {
+    ns[0] = n4p->x;
+    ns[1] = n4p->y;
+    ns[2] = n4p->z;
+  }
+  sre = 0.0;
+  sim = 0.0;
+  if (equation == 0) {
+    double sum = 0.0;
+    if (variant == 0) {
+      double rad = 1.0 / R, pm1 = 1.0, pc = cg;
+      sum = rad;
+      if (p >= 1) {
+        rad *= rho;
+        sum += rad * pc;
+      }
+      for (int n = 1; n < p; ++n) {
+        const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+        pm1 = pc;
+        pc = pn;
+        rad *= rho;
+        sum += rad * pc;
+      }
+    } else if (variant == 1) {
+      const double nt_sh = nt[0] * sh[0] + nt[1] * sh[1] + nt[2] * sh[2];
+      const double nt_th = r > 0.0 ? nt[0] * th[0] + nt[1] * th[1] + nt[2] * th[2] : nt_sh;
+      double rad = 1.0 / (R * R), pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
+      for (int n = 1; n <= p; ++n) {
+        sum += rad * (n * nt_th * pc + (nt_sh - nt_th * cg) * dc);
+        if (n < p) {
+          const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+          const double dn = dm1 + (2 * n + 1) * pc;
+          pm1 = pc;
+          pc = pn;
+          dm1 = dc;
+          dc = dn;
+          rad *= rho;
+        }
+      }
+    } else {
+      const double ns_sh = ns[0] * sh[0] + ns[1] * sh[1] + ns[2] * sh[2];
+      const double ns_th = r > 0.0 ? ns[0] * th[0] + ns[1] * th[1] + ns[2] * th[2] : ns_sh;
+      double rad = 1.0 / (R * R), pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
+      sum = rad * (-1.0 * ns_sh);
+      for (int n = 1; n <= p; ++n) {
+        rad *= rho;
+        sum += rad * (-(n + 1.0) * ns_sh * pc + (ns_th - ns_sh * cg) * dc);
+        if (n < p) {
+          const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+          const double dn = dm1 + (2 * n + 1) * pc;
+          pm1 = pc;
+          pc = pn;
+          dm1 = dc;
+          dc = dn;
+        }
+      }
+    }
+    sre = sum;
+  } else {
+    // h_0..h_{p+1}(kR) upward (_core.pyx:190-193), h'_n (:195-198)
+    double hr[TSQBX_MAX_ORDER + 2], hi[TSQBX_MAX_ORDER + 2];
+    const double x = k * R;
+    double sn, cs;
+    sincos(x, &sn, &cs);
+    hr[0] = sn / x;
+    hi[0] = -cs / x;
+    hr[1] = hr[0] / x + hi[0];   // h0 (1/x - i)
+    hi[1] = hi[0] / x - hr[0];
+    for (int n = 1; n <= p; ++n) {
+      const double f = (2.0 * n + 1.0) / x;
+      hr[n + 1] = f * hr[n] - hr[n - 1];
+      hi[n + 1] = f * hi[n] - hi[n - 1];
+    }
+    double pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
+    const double nt_sh = nt[0] * sh[0] + nt[1] * sh[1] + nt[2] * sh[2];
+    const double nt_th = nt[0] * th[0] + nt[1] * th[1] + nt[2] * th[2];
+    const double ns_sh = ns[0] * sh[0] + ns[1] * sh[1] + ns[2] * sh[2];
+    const double ns_th = r > 0.0 ? ns[0] * th[0] + ns[1] * th[1] + ns[2] * th[2] : ns_sh;
+    for (int n = 0; n <= p; ++n) {
+      const double pn = n == 0 ? 1.0 : pc;
+      const double dn = n == 0 ? 0.0 : dc;
+      if (n >= 1 && n < p) {
+        const double pnx = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
+        const double dnx = dm1 + (2 * n + 1) * pc;
+        pm1 = pc;
+        pc = pnx;
+        dm1 = dc;
+        dc = dnx;
+      }
+      const double tw = 2.0 * n + 1.0;
+      if (variant == 0) {
+        const double f = tw * jt[n] * pn;
+        sre += f * hr[n];
+        sim += f * hi[n];
+      } else if (variant == 1) {
+        double f;
+        if (r > 0.0)
+          f = tw * (k * nt_th * jtp[n] * pn + (nt_sh - nt_th * cg) * jt[n] * dn / r);
+        else
+          f = tw * k * nt_sh * jtp[n] * pn;
+        sre += f * hr[n];
+        sim += f * hi[n];
+      } else {
+        double hpr, hpi;
+        if (n == 0) {
+          hpr = -hr[1];
+          hpi = -hi[1];
+        } else {
+          hpr = hr[n - 1] - (n + 1.0) / x * hr[n];
+          hpi = hi[n - 1] - (n + 1.0) / x * hi[n];
+        }
+        const double f1 = tw * jt[n] * k * ns_sh * pn;
+        const double f2 = tw * jt[n] * (ns_th - ns_sh * cg) * dn / R;
+        sre += f1 * hpr + f2 * hr[n];
+        sim += f1 * hpi + f2 * hi[n];
+      }
+    }
+  }
+}
+
+// Generic kernel: groups of G lanes per center, one target per pass.
 __global__ void __launch_bounds__(128) generic_kernel(const EvalParams a, int equation) {
   const int G = a.G;
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1040,136 +1191,23 @@ __global__ void __launch_bounds__(128) generic_kernel(const EvalParams a, int eq
     const double* jt = equation ? a.ttab + it * a.ttab_stride : nullptr;
     const double* jtp = equation ? jt + (p + 1) : nullptr;
     double accr = 0.0, acci = 0.0, bmax = 0.0;
+    GenericTarget T;
+    for (int d = 0; d < 3; ++d) {
+      T.c[d] = c[d];
+      T.th[d] = th[d];
+      T.nt[d] = nt[d];
+    }
+    T.r = r;
+    T.jt = jt;
+    T.jtp = jtp;
     for (int64_t j = b + lane; j < e; j += G) {
       const int s = a.nidx[j];
       const double4 q4 = a.sp[s];
       const double wim = a.swi[s];
-      const double sc[3] = {q4.x - c[0], q4.y - c[1], q4.z - c[2]};
-      const double R = sqrt(sc[0] * sc[0] + sc[1] * sc[1] + sc[2] * sc[2]);
-      const double sh[3] = {sc[0] / R, sc[1] / R, sc[2] / R};
-      double cg = 1.0;
-      if (r > 0.0) cg = fmin(1.0, fmax(-1.0, sh[0] * th[0] + sh[1] * th[1] + sh[2] * th[2]));
-      const double rho = r / R;
+      double sre, sim, rho;
+      generic_pair(equation, variant, p, k, T, q4, variant == 2 ? a.snrm + s : nullptr, sre, sim,
+                   rho);
       if (a.validate) bmax = fmax(bmax, rho * rho);
-      double ns[3] = {0.0, 0.0, 0.0};
-      if (variant == 2) {
-        const double4 n4 = a.snrm[s];
-        ns[0] = n4.x;
-        ns[1] = n4.y;
-        ns[2] = n4.z;
-      }
-      double sre = 0.0, sim = 0.0;
-      if (equation == 0) {
-        double sum = 0.0;
-        if (variant == 0) {
-          double rad = 1.0 / R, pm1 = 1.0, pc = cg;
-          sum = rad;
-          if (p >= 1) {
-            rad *= rho;
-            sum += rad * pc;
-          }
-          for (int n = 1; n < p; ++n) {
-            const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
-            pm1 = pc;
-            pc = pn;
-            rad *= rho;
-            sum += rad * pc;
-          }
-        } else if (variant == 1) {
-          const double nt_sh = nt[0] * sh[0] + nt[1] * sh[1] + nt[2] * sh[2];
-          const double nt_th = r > 0.0 ? nt[0] * th[0] + nt[1] * th[1] + nt[2] * th[2] : nt_sh;
-          double rad = 1.0 / (R * R), pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
-          for (int n = 1; n <= p; ++n) {
-            sum += rad * (n * nt_th * pc + (nt_sh - nt_th * cg) * dc);
-            if (n < p) {
-              const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
-              const double dn = dm1 + (2 * n + 1) * pc;
-              pm1 = pc;
-              pc = pn;
-              dm1 = dc;
-              dc = dn;
-              rad *= rho;
-            }
-          }
-        } else {
-          const double ns_sh = ns[0] * sh[0] + ns[1] * sh[1] + ns[2] * sh[2];
-          const double ns_th = r > 0.0 ? ns[0] * th[0] + ns[1] * th[1] + ns[2] * th[2] : ns_sh;
-          double rad = 1.0 / (R * R), pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
-          sum = rad * (-1.0 * ns_sh);
-          for (int n = 1; n <= p; ++n) {
-            rad *= rho;
-            sum += rad * (-(n + 1.0) * ns_sh * pc + (ns_th - ns_sh * cg) * dc);
-            if (n < p) {
-              const double pn = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
-              const double dn = dm1 + (2 * n + 1) * pc;
-              pm1 = pc;
-              pc = pn;
-              dm1 = dc;
-              dc = dn;
-            }
-          }
-        }
-        sre = sum;
-      } else {
-        // h_0..h_{p+1}(kR) upward (_core.pyx:190-193), h'_n (:195-198)
-        double hr[TSQBX_MAX_ORDER + 2], hi[TSQBX_MAX_ORDER + 2];
-        const double x = k * R;
-        double sn, cs;
-        sincos(x, &sn, &cs);
-        hr[0] = sn / x;
-        hi[0] = -cs / x;
-        hr[1] = hr[0] / x + hi[0];   // h0 (1/x - i)
-        hi[1] = hi[0] / x - hr[0];
-        for (int n = 1; n <= p; ++n) {
-          const double f = (2.0 * n + 1.0) / x;
-          hr[n + 1] = f * hr[n] - hr[n - 1];
-          hi[n + 1] = f * hi[n] - hi[n - 1];
-        }
-        double pm1 = 1.0, pc = cg, dm1 = 0.0, dc = 1.0;
-        const double nt_sh = nt[0] * sh[0] + nt[1] * sh[1] + nt[2] * sh[2];
-        const double nt_th = nt[0] * th[0] + nt[1] * th[1] + nt[2] * th[2];
-        const double ns_sh = ns[0] * sh[0] + ns[1] * sh[1] + ns[2] * sh[2];
-        const double ns_th = r > 0.0 ? ns[0] * th[0] + ns[1] * th[1] + ns[2] * th[2] : ns_sh;
-        for (int n = 0; n <= p; ++n) {
-          const double pn = n == 0 ? 1.0 : pc;
-          const double dn = n == 0 ? 0.0 : dc;
-          if (n >= 1 && n < p) {
-            const double pnx = ((2 * n + 1) * cg * pc - n * pm1) / (n + 1.0);
-            const double dnx = dm1 + (2 * n + 1) * pc;
-            pm1 = pc;
-            pc = pnx;
-            dm1 = dc;
-            dc = dnx;
-          }
-          const double tw = 2.0 * n + 1.0;
-          if (variant == 0) {
-            const double f = tw * jt[n] * pn;
-            sre += f * hr[n];
-            sim += f * hi[n];
-          } else if (variant == 1) {
-            double f;
-            if (r > 0.0)
-              f = tw * (k * nt_th * jtp[n] * pn + (nt_sh - nt_th * cg) * jt[n] * dn / r);
-            else
-              f = tw * k * nt_sh * jtp[n] * pn;
-            sre += f * hr[n];
-            sim += f * hi[n];
-          } else {
-            double hpr, hpi;
-            if (n == 0) {
-              hpr = -hr[1];
-              hpi = -hi[1];
-            } else {
-              hpr = hr[n - 1] - (n + 1.0) / x * hr[n];
-              hpi = hi[n - 1] - (n + 1.0) / x * hi[n];
-            }
-            const double f1 = tw * jt[n] * k * ns_sh * pn;
-            const double f2 = tw * jt[n] * (ns_th - ns_sh * cg) * dn / R;
-            sre += f1 * hpr + f2 * hr[n];
-            sim += f1 * hpi + f2 * hi[n];
-          }
-        }
-      }
       accr += q4.w * sre - wim * sim;
       acci += q4.w * sim + wim * sre;
     }
@@ -1196,6 +1234,13 @@ __global__ void __launch_bounds__(128) generic_kernel(const EvalParams a, int eq
 // mode 0 (fast S):   tab[n] = (2n+1) j_n(k r) kappa_n,        n <= p
 // mode 1 (generic):  tab[n] = j_n(k r), tab[p+1+n] = j'_n(k r)  (_core.pyx:354-359)
 // ---------------------------------------------------------------------------
+// generic-mode row: j_n, then j'_n (_core.pyx:194-198) from Miller's j (p + 2 values)
+__device__ __forceinline__ void jrow_generic(int p, double x, const double* j, double* row) {
+  for (int n = 0; n <= p; ++n) row[n] = j[n];
+  row[p + 1] = -j[1];
+  for (int n = 1; n <= p; ++n) row[p + 1 + n] = j[n - 1] - (n + 1.0) / x * j[n];
+}
+
 __global__ void helmholtz_target_table(const double* __restrict__ ctr, int64_t n_ctr,
                                        const double* __restrict__ tgt,
                                        const int64_t* __restrict__ tptr, int p, double k,
@@ -1223,9 +1268,7 @@ __global__ void helmholtz_target_table(const double* __restrict__ ctr, int64_t n
           }
         }
       } else {
-        for (int n = 0; n <= p; ++n) row[n] = j[n];
-        row[p + 1] = -j[1];
-        for (int n = 1; n <= p; ++n) row[p + 1 + n] = j[n - 1] - (n + 1.0) / x * j[n];
+        jrow_generic(p, x, j, row);
       }
     } else {
       for (int n = 0; n < stride; ++n) row[n] = 0.0;
@@ -1276,6 +1319,105 @@ __global__ void validate_kernel(const double4* __restrict__ sp, const double* __
       if (R == 0.0) atomicMin(err, base | pos);
       else if (__dmul_rn(R, 1.0 + 1e-12) < r) atomicMin(err, base | (1ull << 31) | pos);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Single call (the reference's per-(center, target) protocol, _core.pyx:205,
+// :310; tsqbx.ts_accumulate): one CTA over one staged buffer
+//   [center(3) target(3) tnormal(3) |t-c|(1) pad(6)] [sp: n x double4] [Im w: n] [pad]
+//   [snrm: n x double4 (D only)]
+// res = {Re, Im, err_key}: the sum with the reference's scaling and, when
+// validating, the exact _prep key ((kind << 31) | position, tsqbx.py:44-53).
+// ---------------------------------------------------------------------------
+constexpr int kOneBlock = 128;
+constexpr int64_t kOneZeroCopyDoubles = 32768;   // 256 KB: below this, read the host buffer in place
+
+__global__ void __launch_bounds__(kOneBlock) one_kernel(int equation, int variant, double k,
+                                                        int p, const double* __restrict__ st,
+                                                        int n, double* __restrict__ res,
+                                                        int validate) {
+  __shared__ double jtab[2 * (TSQBX_MAX_ORDER + 1)];
+  __shared__ double red_r[kOneBlock / 32], red_i[kOneBlock / 32];
+  __shared__ unsigned long long red_k[kOneBlock / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double4* sp = reinterpret_cast<const double4*>(st + 16);
+  const double* swi = st + 16 + 4 * (int64_t)n;
+  const double4* snrm = reinterpret_cast<const double4*>(st + 16 + 4 * (int64_t)n +
+                                                         (((int64_t)n + 3) & ~(int64_t)3));
+  GenericTarget T;
+  const double tc[3] = {st[3] - st[0], st[4] - st[1], st[5] - st[2]};
+  T.r = sqrt(tc[0] * tc[0] + tc[1] * tc[1] + tc[2] * tc[2]);
+  for (int d = 0; d < 3; ++d) {
+    T.c[d] = st[d];
+    T.th[d] = T.r > 0.0 ? tc[d] / T.r : 0.0;
+    T.nt[d] = st[6 + d];
+  }
+  if (equation && tid == 0) {
+    const int stride = 2 * (p + 1);
+    if (T.r > 0.0) {
+      double j[TSQBX_MAX_ORDER + 2];
+      const double x = k * T.r;
+      miller_j(p + 2, x, j);
+      jrow_generic(p, x, j, jtab);
+    } else {
+      for (int m = 0; m < stride; ++m) jtab[m] = 0.0;
+      jtab[0] = 1.0;
+      if (p >= 1) jtab[p + 2] = 1.0 / 3.0;     // j'_1(0) = 1/3 (_core.pyx:357-359)
+    }
+  }
+  T.jt = jtab;
+  T.jtp = jtab + (p + 1);
+  __syncthreads();
+  // |t - c| exactly as the caller's _prep formed it (numpy's 1-D norm is a dot
+  // product whose rounding is the host's business), staged in slot 9
+  const double rref = st[9];
+  double accr = 0.0, acci = 0.0;
+  unsigned long long key = (unsigned long long)TSQBX_ERR_KEY_NONE;
+  for (int j = tid; j < n; j += kOneBlock) {
+    const double4 q4 = sp[j];
+    const double wim = swi[j];
+    double sre, sim, rho;
+    generic_pair(equation, variant, p, k, T, q4, variant == 2 ? snrm + j : nullptr, sre, sim, rho);
+    accr += q4.w * sre - wim * sim;
+    acci += q4.w * sim + wim * sre;
+    if (validate) {
+      const double R = norm_ref(__dadd_rn(q4.x, -st[0]), __dadd_rn(q4.y, -st[1]),
+                                __dadd_rn(q4.z, -st[2]));
+      unsigned long long kj = (unsigned long long)TSQBX_ERR_KEY_NONE;
+      if (R == 0.0) kj = (unsigned long long)j;
+      else if (__dmul_rn(R, 1.0 + 1e-12) < rref) kj = (1ull << 31) | (unsigned long long)j;
+      key = kj < key ? kj : key;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    accr += __shfl_xor_sync(0xffffffffu, accr, off);
+    acci += __shfl_xor_sync(0xffffffffu, acci, off);
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, off);
+    key = ok < key ? ok : key;
+  }
+  if (lane == 0) {
+    red_r[wid] = accr;
+    red_i[wid] = acci;
+    red_k[wid] = key;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    accr = acci = 0.0;
+    for (int w = 0; w < kOneBlock / 32; ++w) {
+      accr += red_r[w];
+      acci += red_i[w];
+      key = red_k[w] < key ? red_k[w] : key;
+    }
+    if (equation == 0) {
+      res[0] = accr / kFourPi;
+      res[1] = acci / kFourPi;
+    } else {
+      const double pk = k / kFourPi;
+      res[0] = -acci * pk;
+      res[1] = accr * pk;
+    }
+    reinterpret_cast<unsigned long long*>(res)[2] = key;
   }
 }
 
@@ -1624,6 +1766,55 @@ int tsqbx_validate(const double* packed, int64_t n_src, const double* ctr_xyz, i
                                             tgt_ptr, (unsigned long long*)err_key);
   }
   return check_cuda(cudaGetLastError(), "validate launch");
+}
+
+int64_t tsqbx_one_staging_doubles(int64_t n_src, int with_normals) {
+  return 16 + 4 * n_src + ((n_src + 3) & ~(int64_t)3) + (with_normals ? 4 * n_src : 0);
+}
+
+int tsqbx_eval_one(int equation, int variant, double k, int p, const double* staged_host,
+                   int64_t n_src, unsigned flags, double* device_buf, int64_t device_doubles,
+                   double* result_host, void* stream) {
+  if (equation != TSQBX_EQ_LAPLACE && equation != TSQBX_EQ_HELMHOLTZ)
+    return set_error(TSQBX_ERR_ARGUMENT, "eval_one: bad equation %d", equation);
+  if (variant < 0 || variant > 2) return set_error(TSQBX_ERR_ARGUMENT, "eval_one: bad variant");
+  if (p < 0 || p > TSQBX_MAX_ORDER) return set_error(TSQBX_ERR_ARGUMENT, "eval_one: bad order");
+  if (n_src < 0 || n_src > INT32_MAX || !staged_host || !device_buf || !result_host)
+    return set_error(TSQBX_ERR_ARGUMENT, "eval_one: bad arguments");
+  if (equation == TSQBX_EQ_HELMHOLTZ && !(k > 0.0))
+    return set_error(TSQBX_ERR_ARGUMENT, "eval_one: Helmholtz needs k > 0");
+  const int64_t nd = tsqbx_one_staging_doubles(n_src, variant == TSQBX_VARIANT_D);
+  if (device_doubles < nd + 4) return set_error(TSQBX_ERR_ARGUMENT, "eval_one: device buffer too small");
+  const cudaStream_t st = (cudaStream_t)stream;
+  // small batches: the kernel reads the pinned staging buffer and writes the
+  // result in place over PCIe (mapped pinned memory under UVA) -- no copies
+  if (nd <= kOneZeroCopyDoubles) {
+    cudaPointerAttributes in{}, out{};
+    if (cudaPointerGetAttributes(&in, staged_host) == cudaSuccess &&
+        cudaPointerGetAttributes(&out, result_host) == cudaSuccess &&
+        in.type == cudaMemoryTypeHost && out.type == cudaMemoryTypeHost && in.devicePointer &&
+        out.devicePointer) {
+      one_kernel<<<1, kOneBlock, 0, st>>>(equation, variant, k, p,
+                                          static_cast<const double*>(in.devicePointer),
+                                          (int)n_src, static_cast<double*>(out.devicePointer),
+                                          (flags & TSQBX_FLAG_VALIDATE) ? 1 : 0);
+      const cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) return check_cuda(le, "one_kernel launch");
+      return check_cuda(cudaStreamSynchronize(st), "eval_one sync");
+    }
+    cudaGetLastError();   // not pinned: fall through to the copies
+  }
+  cudaError_t e = cudaMemcpyAsync(device_buf, staged_host, nd * sizeof(double),
+                                  cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "eval_one H2D");
+  double* dres = device_buf + ((nd + 3) & ~(int64_t)3);
+  one_kernel<<<1, kOneBlock, 0, st>>>(equation, variant, k, p, device_buf, (int)n_src, dres,
+                                      (flags & TSQBX_FLAG_VALIDATE) ? 1 : 0);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return check_cuda(e, "one_kernel launch");
+  e = cudaMemcpyAsync(result_host, dres, 3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return check_cuda(e, "eval_one D2H");
+  return check_cuda(cudaStreamSynchronize(st), "eval_one sync");
 }
 
 }  // extern "C"

@@ -345,32 +345,53 @@ class TsqbxProblem:
 
 def ts_accumulate(cfg: TsConfig, sources, weights, center, target,
                   source_normals=None, target_normal=None) -> complex:
-    """sum_j w_j * (p-th order target-specific expansion of source j)  (tsqbx.py:68-80)."""
+    """sum_j w_j * (p-th order target-specific expansion of source j)  (tsqbx.py:68-80).
+
+    Same checks, in the same order, as the reference's ``_prep``
+    (tsqbx.py:38-65): coincident source, separation, then the normals.  The
+    geometric checks run exactly inside the single-call kernel; the value comes
+    from the same launch (one H2D copy, one kernel, one D2H copy)."""
+    from ._single import one_call
+
     sources = np.ascontiguousarray(sources, dtype=np.float64).reshape(-1, 3)
     weights = np.ascontiguousarray(weights, dtype=np.complex128).reshape(-1)
-    center = np.asarray(center, dtype=np.float64).reshape(1, 3)
-    target = np.asarray(target, dtype=np.float64).reshape(1, 3)
-    if cfg.spec.needs_source_normals and source_normals is None:
-        raise ValueError("double-layer variant requires source normals")
-    if cfg.spec.needs_target_normals and target_normal is None:
-        raise ValueError("S' variant requires a target normal")
+    center = np.asarray(center, dtype=np.float64).reshape(3)
+    target = np.asarray(target, dtype=np.float64).reshape(3)
+    spec = cfg.spec
+    need_sn = spec.needs_source_normals and source_normals is None
+    need_tn = spec.needs_target_normals and target_normal is None
+    r = float(np.linalg.norm(target - center))
     n = sources.shape[0]
-    if n == 0:
+    if need_sn or need_tn or n == 0:
+        _prep_geometry(sources, center, r)          # geometry errors come first
+        if need_sn:
+            raise ValueError("double-layer variant requires source normals")
+        if need_tn:
+            raise ValueError("S' variant requires a target normal")
         return 0.0 + 0.0j
-    dev = dv.require_cuda()
-    src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, center, target, source_normals,
-                                       None if target_normal is None else
-                                       np.asarray(target_normal, dtype=np.float64).reshape(1, 3),
-                                       dev)
-    near = NearLists(n_ctr=1, n_src=n, n_pairs=n,
-                     ptr=torch.tensor([0, n], dtype=torch.int64, device=dev),
-                     csr_idx=torch.arange(n, dtype=torch.int32, device=dev))
-    tptr = torch.tensor([0, 1], dtype=torch.int64, device=dev)
-    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr)
-    out = torch.empty(1, dtype=torch.complex128, device=dev)
-    prep.launch(torch.view_as_real(out), validate=True)
-    prep.check_errors(batch_context=False)
-    return complex(out.cpu().numpy()[0])
+    sn = (np.ascontiguousarray(source_normals, dtype=np.float64).reshape(-1, 3)
+          if spec.needs_source_normals else None)
+    tn = (np.asarray(target_normal, dtype=np.float64).reshape(3)
+          if spec.needs_target_normals else None)
+    value, key = one_call(_equation_code(spec), spec.variant_code, float(spec.helmholtz_k or 0.0),
+                          cfg.p_qbx, sources, weights, sn, center, target, tn, validate=True,
+                          r_ref=r)
+    if key != _lib.ERR_KEY_NONE:
+        _prep_geometry(sources, center, r)          # names the source like the reference
+        raise RuntimeError(f"device validation key {key:#x} not reproduced on the host")
+    return value
+
+
+def _prep_geometry(sources, center, r):
+    """The reference's geometric checks and messages (tsqbx.py:42-51)."""
+    R = np.linalg.norm(sources - center, axis=1)
+    if np.any(R == 0.0):
+        raise ValueError(f"source {int(np.argmin(R))} coincides with the expansion center")
+    viol = R * (1.0 + _SEP_SLACK) < r
+    if np.any(viol):
+        bad = int(np.argmax(viol))
+        raise ValueError(
+            f"separation violation for source {bad}: |t-c| = {r} exceeds |s-c| = {R[bad]}")
 
 
 def ts_eval(cfg: TsConfig, source, center, target, source_normal=None,
