@@ -1,0 +1,39 @@
+"""Host-side behaviour of the public API that needs no GPU: argument checks in
+the reference's order (tsqbx.py:38-65, kernels.py:44-71)."""
+
+import numpy as np
+import pytest
+
+from paper_1811_01110_b200 import KernelSpec, TsConfig, ts_accumulate
+from paper_1811_01110_b200.kernels import Equation, Variant
+
+D = KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV)
+SP = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=2.0, variant=Variant.TARGET_NORMAL_DERIV)
+
+
+def test_geometry_errors_precede_missing_normals():
+    # _prep checks coincidence, then separation, then the normals
+    with pytest.raises(ValueError, match="source 1 coincides"):
+        ts_accumulate(TsConfig(D, 4), [[1.0, 0, 0], [0, 0, 0]], [1, 1], np.zeros(3),
+                      [0.1, 0, 0])
+    with pytest.raises(ValueError, match="separation violation for source 0"):
+        ts_accumulate(TsConfig(SP, 4), [[0.1, 0, 0]], [1], np.zeros(3), [0.5, 0, 0])
+
+
+def test_missing_normals_and_empty_batches():
+    with pytest.raises(ValueError, match="double-layer variant requires source normals"):
+        ts_accumulate(TsConfig(D, 4), np.zeros((0, 3)), [], np.zeros(3), np.zeros(3))
+    with pytest.raises(ValueError, match="S' variant requires a target normal"):
+        ts_accumulate(TsConfig(SP, 4), [[0, 0, 2.0]], [1], np.zeros(3), [0.1, 0, 0])
+    assert ts_accumulate(TsConfig(KernelSpec(), 4), np.zeros((0, 3)), [], np.zeros(3),
+                         np.zeros(3)) == 0
+
+
+def test_kernelspec_validation():
+    # kernels.py:50-55
+    with pytest.raises(ValueError, match="Helmholtz requires"):
+        KernelSpec(equation=Equation.HELMHOLTZ)
+    with pytest.raises(ValueError, match="only valid for the Helmholtz"):
+        KernelSpec(helmholtz_k=1.0)
+    with pytest.raises(ValueError, match="nonnegative"):
+        TsConfig(KernelSpec(), -1)
