@@ -252,6 +252,33 @@ __global__ void p2p_reduce_kernel(const double2* __restrict__ part, int64_t chun
     atomicMin(err, (unsigned long long)TSQBX_ERR_KEY_SUSPECT);
 }
 
+// Many chunks, few targets: a warp per target, lane l adds chunks l, l+32, ...
+// and a fixed shuffle tree combines the lanes (deterministic).
+__global__ void p2p_reduce_warp_kernel(const double2* __restrict__ part, int64_t chunks,
+                                       int64_t n_tgt, double2* __restrict__ out, int screen,
+                                       unsigned long long* err) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= n_tgt) return;
+  double ar = 0.0, ai = 0.0;
+  for (int64_t c = lane; c < chunks; c += 32) {
+    const double2 v = part[c * n_tgt + t];
+    ar += v.x;
+    ai += v.y;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, off);
+    ai += __shfl_xor_sync(0xffffffffu, ai, off);
+  }
+  if (lane == 0) {
+    ar *= kInvFourPi;
+    ai *= kInvFourPi;
+    out[t] = make_double2(ar, ai);
+    if (screen && !(isfinite(ar) && isfinite(ai)))
+      atomicMin(err, (unsigned long long)TSQBX_ERR_KEY_SUSPECT);
+  }
+}
+
 // Exact singular-pair search (r2 == 0; the fused and unfused sums of squares
 // vanish together): key = (target << 32) | source, minimised.
 __global__ void p2p_singular_kernel(const double4* __restrict__ sp, int64_t n_src,
@@ -311,15 +338,17 @@ struct P2PPlan {
   int64_t chunks, chunk_len, blocks_x;
 };
 
-// dense: TT = min(128, pow2 >= n_tgt); enough (tile, chunk) CTAs for ~8 per SM,
-// each chunk >= 2048 sources.  rows: TT from the mean targets per row.
-P2PPlan p2p_plan(int64_t n_src, int64_t n_tgt, int64_t n_rows, bool dense) {
+// dense: TT = min(128, pow2 >= n_tgt); the sources are split into chunks
+// (blockIdx.y) so that tiles x chunks fills whole waves of the kernel's
+// resident CTAs (`slots`; 0 = unknown, size for the largest choice), each chunk
+// >= 1024 sources.  rows: TT from the mean targets per row.
+P2PPlan p2p_plan(int64_t n_src, int64_t n_tgt, int64_t n_rows, bool dense, int64_t slots) {
   P2PPlan p{};
   p.tpt = 1;
   if (dense) {
     p.log2_tt = std::min(7, ilog2_ceil(std::max<int64_t>(n_tgt, 1)));
     const int64_t want = 8LL * sm_count();
-    const int64_t max_chunks = std::max<int64_t>(1, n_src / 2048);
+    const int64_t max_chunks = std::max<int64_t>(1, n_src / 1024);
     // enough targets (with source chunks still filling the machine): 4 per
     // thread -- independent FP64 chains and 4x fewer shared-memory reads
     const int64_t per4 = (int64_t)kP2PTpt * kP2PBlock;
@@ -327,8 +356,25 @@ P2PPlan p2p_plan(int64_t n_src, int64_t n_tgt, int64_t n_rows, bool dense) {
       p.tpt = kP2PTpt;
     const int64_t per = (int64_t)p.tpt << p.log2_tt;
     const int64_t tiles = (n_tgt + per - 1) / per;
-    p.chunks = std::max<int64_t>(1, std::min(max_chunks, (want + tiles - 1) / std::max<int64_t>(tiles, 1)));
-    p.chunk_len = (n_src + p.chunks - 1) / p.chunks;
+    const int64_t sl = slots > 0 ? slots : 16LL * sm_count();     // 16 = 2048 / 128 threads
+    int64_t chunks = 1;
+    if (tiles < sl) {
+      const int64_t cmax = std::max<int64_t>(1, std::min(max_chunks, (2 * sl + tiles - 1) / tiles));
+      if (slots <= 0) {
+        chunks = cmax;                                 // sizing: the largest possible choice
+      } else {
+        double best = -1.0;
+        for (int64_t c = 1; c <= cmax; ++c) {
+          const double x = (double)(tiles * c) / (double)sl;
+          const double score = x / std::ceil(x) * std::min(1.0, x);
+          if (score > best + 1e-3) {
+            best = score;
+            chunks = c;
+          }
+        }
+      }
+    }
+    p.chunk_len = (n_src + chunks - 1) / chunks;
     p.chunk_len = std::max<int64_t>(kP2PBlock, (p.chunk_len + kP2PBlock - 1) / kP2PBlock * kP2PBlock);
     p.chunks = std::max<int64_t>(1, (n_src + p.chunk_len - 1) / p.chunk_len);
     p.blocks_x = tiles;
@@ -340,6 +386,34 @@ P2PPlan p2p_plan(int64_t n_src, int64_t n_tgt, int64_t n_rows, bool dense) {
     p.blocks_x = n_rows;
   }
   return p;
+}
+
+// resident CTAs of the p2p kernel instance the plan will launch
+template <int EQ, int VARIANT>
+int64_t p2p_slots(bool tpt4, bool precise) {
+  int nb = 0;
+  cudaError_t e;
+  if (tpt4)
+    e = precise ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p2p_kernel<EQ, VARIANT, true, kP2PTpt>, kP2PBlock, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p2p_kernel<EQ, VARIANT, false, kP2PTpt>, kP2PBlock, 0);
+  else
+    e = precise ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p2p_kernel<EQ, VARIANT, true, 1>, kP2PBlock, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p2p_kernel<EQ, VARIANT, false, 1>, kP2PBlock, 0);
+  if (e != cudaSuccess || nb <= 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (int64_t)nb * sm_count();
+}
+
+int64_t slots_for(int equation, int variant, bool tpt4, bool precise) {
+  if (equation == TSQBX_EQ_LAPLACE)
+    return variant == 0 ? p2p_slots<TSQBX_EQ_LAPLACE, 0>(tpt4, precise)
+         : variant == 1 ? p2p_slots<TSQBX_EQ_LAPLACE, 1>(tpt4, precise)
+                        : p2p_slots<TSQBX_EQ_LAPLACE, 2>(tpt4, precise);
+  return variant == 0 ? p2p_slots<TSQBX_EQ_HELMHOLTZ, 0>(tpt4, precise)
+       : variant == 1 ? p2p_slots<TSQBX_EQ_HELMHOLTZ, 1>(tpt4, precise)
+                      : p2p_slots<TSQBX_EQ_HELMHOLTZ, 2>(tpt4, precise);
 }
 
 template <int EQ, int VARIANT>
@@ -363,7 +437,7 @@ using namespace tsqbx;
 extern "C" {
 
 int64_t tsqbx_p2p_workspace_bytes(int64_t n_src, int64_t n_tgt, int64_t n_rows, int dense) {
-  const P2PPlan pl = p2p_plan(n_src, n_tgt, n_rows, dense != 0);
+  const P2PPlan pl = p2p_plan(n_src, n_tgt, n_rows, dense != 0, 0);
   return pl.chunks > 1 ? pl.chunks * n_tgt * 2 * (int64_t)sizeof(double) : 0;
 }
 
@@ -401,7 +475,10 @@ int tsqbx_p2p_packed(int equation, int variant, double k, const double* packed, 
   }
   if (!packed || (((uintptr_t)packed) & 31))
     return set_error(TSQBX_ERR_ARGUMENT, "p2p: packed sources must be 32-byte aligned");
-  const P2PPlan pl = p2p_plan(n_src, n_tgt, n_rows, dense);
+  const bool precise = (flags & TSQBX_FLAG_PRECISE) != 0;
+  P2PPlan pl = p2p_plan(n_src, n_tgt, n_rows, dense, 0);
+  if (dense) pl = p2p_plan(n_src, n_tgt, n_rows, dense,
+                           slots_for(equation, variant, pl.tpt == kP2PTpt && kP2PTpt > 1, precise));
   if (pl.blocks_x > INT32_MAX || pl.chunks > 65535)
     return set_error(TSQBX_ERR_ARGUMENT, "p2p: grid too large");
   const int64_t need = tsqbx_p2p_workspace_bytes(n_src, n_tgt, n_rows, dense);
@@ -431,7 +508,6 @@ int tsqbx_p2p_packed(int equation, int variant, double k, const double* packed, 
   a.log2_tt = pl.log2_tt;
   a.screen = (flags & TSQBX_FLAG_VALIDATE) ? 1 : 0;
   a.k = k;
-  const bool precise = (flags & TSQBX_FLAG_PRECISE) != 0;
 
   int rc;
   if (equation == TSQBX_EQ_LAPLACE) {
@@ -445,9 +521,14 @@ int tsqbx_p2p_packed(int equation, int variant, double k, const double* packed, 
   }
   if (rc || pl.chunks == 1) return rc;
   const int blocks = (int)((n_tgt + 255) / 256);
-  p2p_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(a.part), pl.chunks,
-                                            n_tgt, reinterpret_cast<double2*>(out), a.screen,
-                                            a.err);
+  if (pl.chunks >= 64 && n_tgt * 32 <= 8LL * 256 * sm_count())
+    p2p_reduce_warp_kernel<<<(unsigned)((n_tgt * 32 + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const double2*>(a.part), pl.chunks, n_tgt,
+        reinterpret_cast<double2*>(out), a.screen, a.err);
+  else
+    p2p_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(a.part), pl.chunks,
+                                              n_tgt, reinterpret_cast<double2*>(out), a.screen,
+                                              a.err);
   return check_cuda(cudaGetLastError(), "p2p_reduce launch");
 }
 
