@@ -11,9 +11,9 @@ stage is two launches:
 * the box lists are expanded on the device into per-row source index lists
   (``tsqbx_box_rows_count/fill``, csrc/boxes.cu): one row per QBX center and
   one row per target box for the conventional targets;
-* the centers go through the TSQBX evaluator (``ts_accumulate_batch``, the
-  hot path -- SELL layout, fast kernels), the conventional targets through the
-  p2p row kernel (``P2PProblem.evaluate(rows=...)``).
+* the centers go through the TSQBX evaluator (a ``TsqbxProblem``: the hot
+  path, SELL layout, fast kernels), the conventional targets through the p2p
+  row kernel (``P2PProblem.evaluate(rows=...)``).
 
 Everything is in the tree's point order, exactly as the driver holds it
 (``tree.points[SOURCES]``, permuted weights and normals, ``qcenters`` /
@@ -33,7 +33,7 @@ from . import _lib
 from .kernels import KernelSpec
 from .nearlist import NearLists
 from .p2p import P2PProblem
-from .tsqbx import TsConfig, ts_accumulate_batch
+from .tsqbx import TsConfig, TsqbxProblem
 
 SOURCES, TARGETS, CENTERS = 0, 1, 2      # tree.py:26-28
 
@@ -90,6 +90,12 @@ class DirectStage:
     ``source_normals`` the permuted normals (D only), ``qtargets`` /
     ``qnormals`` the targets (and S' normals) of the tree-ordered centers,
     ``conv_normals`` the conventional targets' normals (S' only).
+
+    The expansion of a list into row index lists, its SELL copy and the
+    prepared TSQBX / p2p problems are built on the first ``run`` of that list
+    and kept: the driver re-evaluates the same tree for every GMRES matvec
+    (``prepared``, driver.py:118-122), so later calls only repack the sources
+    when ``set_weights`` gave a new density and launch the two kernels.
     """
 
     def __init__(self, spec: KernelSpec, p_qbx: int, tree, target_boxes, weights,
@@ -125,36 +131,63 @@ class DirectStage:
         self.row_tgt, self.tbox = _owner_rows(owned_start, owned_end, TARGETS, n_t, is_tb)
         self.p2p = (P2PProblem(spec, self.sources, self.weights, self.snormals, dev)
                     if n_t else None)
+        self._plans = {}
+        self._version = 0
+
+    def set_weights(self, weights) -> None:
+        """A new (permuted) density for the same tree: sources are repacked lazily."""
+        self.weights = dv.to_device(weights, torch.complex128, self.dev, (-1,))
+        if self.p2p is not None:
+            self.p2p.set_weights(self.weights)
+        self._version += 1
+
+    def _plan(self, list_csr):
+        key = id(list_csr)
+        plan = self._plans.get(key)
+        if plan is not None and plan["list"] is list_csr:
+            return plan
+        starts, flat = (list_csr.starts, list_csr.flat) if hasattr(list_csr, "starts") \
+            else list_csr
+        dev = self.dev
+        n_c = int(self.qcenters.shape[0])
+        plan = {"list": list_csr, "prob": None, "rows": None, "nts": 0, "version": self._version}
+        if n_c:
+            ptr, idx = box_rows(self.center_box, starts, flat, self.box_src_start,
+                                self.box_src_end, dev)
+            plan["nts"] = int(idx.shape[0])
+            if plan["nts"]:
+                near = NearLists(n_ctr=n_c, n_src=int(self.sources.shape[0]),
+                                 n_pairs=plan["nts"], ptr=ptr, csr_idx=idx)
+                plan["prob"] = TsqbxProblem(self.cfg, self.sources, self.weights, self.qcenters,
+                                            self.qtargets, near, source_normals=self.snormals,
+                                            target_normals=self.qnormals, device=dev)
+        if self.p2p is not None and self.tbox.size:
+            rptr, ridx = box_rows(self.tbox, starts, flat, self.box_src_start,
+                                  self.box_src_end, dev)
+            if int(ridx.shape[0]):
+                plan["rows"] = self.p2p.rows(self.row_tgt, rptr, ridx, int(self.conv.shape[0]))
+        self._plans[key] = plan
+        return plan
 
     def run(self, list_csr):
         """(conv_near, qbx_near_val, ts_pairs): the stage's additions to the
         driver's accumulators (complex128 CUDA tensors over the tree-ordered
         conventional targets and centers) and the ``counts["ts"]`` increment."""
-        starts, flat = (list_csr.starts, list_csr.flat) if hasattr(list_csr, "starts") \
-            else list_csr
+        plan = self._plan(list_csr)
         dev = self.dev
-        n_c = int(self.qcenters.shape[0])
-        conv_add = torch.zeros(int(self.conv.shape[0]), dtype=torch.complex128, device=dev)
-        qbx_add = torch.zeros(n_c, dtype=torch.complex128, device=dev)
-        ts_pairs = 0
-        if n_c:
-            ptr, idx = box_rows(self.center_box, starts, flat, self.box_src_start,
-                                self.box_src_end, dev)
-            ts_pairs = int(idx.shape[0])
-            if ts_pairs:
-                near = NearLists(n_ctr=n_c, n_src=int(self.sources.shape[0]),
-                                 n_pairs=ts_pairs, ptr=ptr, csr_idx=idx)
-                qbx_add = ts_accumulate_batch(self.cfg, self.sources, self.weights,
-                                              self.qcenters, self.qtargets, near,
-                                              source_normals=self.snormals,
-                                              target_normals=self.qnormals, validate=False,
-                                              device=dev)
-        if self.p2p is not None and self.tbox.size:
-            rptr, ridx = box_rows(self.tbox, starts, flat, self.box_src_start,
-                                  self.box_src_end, dev)
-            if int(ridx.shape[0]):
-                # the reference's p2p raises on a coincident pair even inside the
-                # driver (_core.pyx:109-111), so this one is screened
-                conv_add = self.p2p.evaluate(self.conv, self.conv_normals,
-                                             rows=(self.row_tgt, rptr, ridx), validate=True)
-        return conv_add, qbx_add, ts_pairs
+        if plan["prob"] is not None:
+            if plan["version"] != self._version:
+                plan["prob"].set_weights(self.weights)
+                plan["version"] = self._version
+            qbx_add = plan["prob"].evaluate(validate=False).clone()
+        else:
+            qbx_add = torch.zeros(int(self.qcenters.shape[0]), dtype=torch.complex128,
+                                  device=dev)
+        if plan["rows"] is not None:
+            # the reference's p2p raises on a coincident pair even inside the
+            # driver (_core.pyx:109-111), so this one is screened
+            conv_add = self.p2p.evaluate(self.conv, self.conv_normals, rows=plan["rows"],
+                                         validate=True)
+        else:
+            conv_add = torch.zeros(int(self.conv.shape[0]), dtype=torch.complex128, device=dev)
+        return conv_add, qbx_add, plan["nts"]

@@ -16,12 +16,25 @@ target i, source j")`` for the first pair in target-major order.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
 from . import _device as dv
 from . import _lib
 from .kernels import KernelSpec
+
+
+@dataclass
+class P2PRows:
+    """Device row structure for ``P2PProblem.evaluate`` (checked once)."""
+
+    row_tgt: torch.Tensor
+    row_ptr: torch.Tensor
+    row_idx: torch.Tensor
+    n_rows: int
+    n_tgt: int
 
 
 class P2PProblem:
@@ -45,12 +58,42 @@ class P2PProblem:
             sn = dv.to_device(source_normals, torch.float64, self.dev, (-1, 3))
         self.n_src = int(src.shape[0])
         self.with_normals = sn is not None
+        self.src, self.sn = src, sn
         nd = int(L.tsqbx_packed_doubles(self.n_src, int(self.with_normals)))
         self.packed = torch.empty(nd, dtype=torch.float64, device=self.dev)
-        _lib.check(L.tsqbx_pack_sources(self.n_src, src.data_ptr(), w.data_ptr(), dv.ptr(sn),
-                                        None, self.packed.data_ptr(),
-                                        dv.stream_handle(self.dev)), "tsqbx_pack_sources")
+        self._pack(w)
         self.err = torch.empty(1, dtype=torch.int64, device=self.dev)
+
+    def _pack(self, w: torch.Tensor) -> None:
+        L = _lib.load()
+        _lib.check(L.tsqbx_pack_sources(self.n_src, self.src.data_ptr(), w.data_ptr(),
+                                        dv.ptr(self.sn), None, self.packed.data_ptr(),
+                                        dv.stream_handle(self.dev)), "tsqbx_pack_sources")
+
+    def set_weights(self, weights) -> None:
+        """New source weights (same sources): one pack kernel, no reallocation."""
+        if isinstance(weights, torch.Tensor) and not weights.is_complex():
+            weights = weights.to(torch.complex128)
+        w = dv.complex_as_f64(dv.to_device(weights, torch.complex128, self.dev, (-1,)))
+        if w.shape[0] != self.n_src:
+            raise ValueError("weights must have one entry per source")
+        self._pack(w)
+
+    def rows(self, row_tgt, row_ptr, row_idx, n_tgt: int) -> "P2PRows":
+        """Checked device copy of a row structure for repeated ``evaluate``."""
+        rt = dv.to_device(row_tgt, torch.int64, self.dev, (-1,))
+        rp = dv.to_device(row_ptr, torch.int64, self.dev, (-1,))
+        ri = dv.to_device(row_idx, torch.int32, self.dev, (-1,))
+        n_rows = int(rt.shape[0]) - 1
+        if n_rows < 0 or rp.shape[0] != n_rows + 1:
+            raise ValueError("row_tgt and row_ptr must both have n_rows + 1 entries")
+        if n_rows > 0:
+            ends = torch.stack([rt[0], rt[-1], rp[0], rp[-1]]).cpu().tolist()
+            if ends[0] != 0 or ends[1] != n_tgt or ends[2] != 0 or ends[3] > ri.shape[0]:
+                raise ValueError("rows must partition the targets and index row_idx")
+        elif n_tgt:
+            raise ValueError("rows must partition the targets")
+        return P2PRows(rt, rp, ri, n_rows, n_tgt)
 
     def _targets(self, targets, target_normals):
         tgt = dv.to_device(targets, torch.float64, self.dev, (-1, 3))
@@ -73,18 +116,11 @@ class P2PProblem:
         rt = rp = ri = None
         n_rows = 0
         if rows is not None:
-            rt = dv.to_device(rows[0], torch.int64, self.dev, (-1,))
-            rp = dv.to_device(rows[1], torch.int64, self.dev, (-1,))
-            ri = dv.to_device(rows[2], torch.int32, self.dev, (-1,))
-            n_rows = int(rt.shape[0]) - 1
-            if n_rows < 0 or rp.shape[0] != n_rows + 1:
-                raise ValueError("row_tgt and row_ptr must both have n_rows + 1 entries")
-            if n_rows > 0:
-                ends = torch.stack([rt[0], rt[-1], rp[0], rp[-1]]).cpu().tolist()
-                if ends[0] != 0 or ends[1] != n_tgt or ends[2] != 0 or ends[3] > ri.shape[0]:
-                    raise ValueError("rows must partition the targets and index row_idx")
-            elif n_tgt:
-                raise ValueError("rows must partition the targets")
+            if not isinstance(rows, P2PRows):
+                rows = self.rows(rows[0], rows[1], rows[2], n_tgt)
+            elif rows.n_tgt != n_tgt:
+                raise ValueError("rows were prepared for a different number of targets")
+            rt, rp, ri, n_rows = rows.row_tgt, rows.row_ptr, rows.row_idx, rows.n_rows
         if out is None:
             out = torch.empty(n_tgt, dtype=torch.complex128, device=self.dev)
         o = torch.view_as_real(out)

@@ -99,10 +99,7 @@ class _Prepared:
         st = dv.stream_handle(dev)
         nd = int(L.tsqbx_packed_doubles(self.n_src, self.with_normals))
         self.packed = torch.empty(max(nd, 4), dtype=torch.float64, device=dev)
-        _lib.check(L.tsqbx_pack_sources(self.n_src, dv.ptr(src), dv.ptr(w),
-                                        dv.ptr(sn) if self.with_normals else None,
-                                        dv.ptr(near.src_perm), self.packed.data_ptr(), st),
-                   "tsqbx_pack_sources")
+        self.pack(w)
         tn = tn if self.variant == 1 else None
         if near.ctr_order is None:
             self.ctr, self.tptr, self.tgt, self.tn, self.tidx = ctr, tptr, tgt, tn, None
@@ -132,6 +129,17 @@ class _Prepared:
         # and the kernel picks its real-weight path itself (no host round trip)
         self.real_w = False
         self.one_target = os.environ.get("GIGAQBX_ONE_TARGET", "0") == "1"
+
+    def pack(self, w: torch.Tensor) -> None:
+        """(Re)pack the sources with weights ``w`` (interleaved float64 view)."""
+        L = _lib.load()
+        if w.shape[0] != self.n_src:
+            raise ValueError("weights must have one entry per source")
+        self.w = w
+        _lib.check(L.tsqbx_pack_sources(self.n_src, dv.ptr(self.src), dv.ptr(w),
+                                        dv.ptr(self.sn) if self.with_normals else None,
+                                        dv.ptr(self.near.src_perm), self.packed.data_ptr(),
+                                        dv.stream_handle(self.dev)), "tsqbx_pack_sources")
 
     def launch(self, out: torch.Tensor, validate: bool, generic: bool = False,
                rows: tuple[int, int] | None = None, out_offset: int = 0,
@@ -319,6 +327,13 @@ class TsqbxProblem:
         self.prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
         self.out = torch.empty(self.prep.n_tgt, dtype=torch.complex128, device=dev)
         self.n_pairs_per_target = None
+
+    def set_weights(self, weights) -> None:
+        """New densities for the same geometry (GMRES matvecs): one pack kernel."""
+        if isinstance(weights, torch.Tensor) and not weights.is_complex():
+            weights = weights.to(torch.complex128)
+        self.prep.pack(dv.complex_as_f64(dv.to_device(weights, torch.complex128,
+                                                      self.prep.dev, (-1,))))
 
     @property
     def group_lanes(self) -> int:

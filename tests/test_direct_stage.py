@@ -102,3 +102,10 @@ def test_gpu_direct_stage_matches_reference(g, kname):
         assert nts == int(g[f"{lname}_{kname}_nts"])
         assert normwise(qbx.cpu().numpy(), g[f"{lname}_{kname}_qbx"]) <= tol
         assert normwise(conv.cpu().numpy(), g[f"{lname}_{kname}_conv"]) <= tol
+    # GMRES-style reuse: a new density on the cached plans (linear in the weights)
+    ds.set_weights((2.0 - 0.5j) * g["weights"])
+    for lname in LISTS:
+        conv, qbx, _ = ds.run(SimpleNamespace(starts=g[f"{lname}_starts"],
+                                              flat=g[f"{lname}_flat"]))
+        assert normwise(qbx.cpu().numpy(), (2.0 - 0.5j) * g[f"{lname}_{kname}_qbx"]) <= tol
+        assert normwise(conv.cpu().numpy(), (2.0 - 0.5j) * g[f"{lname}_{kname}_conv"]) <= tol
