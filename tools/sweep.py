@@ -17,8 +17,18 @@ ap.add_argument("--cases", default="c2/dense,c2/literal,c3/dense,c3/literal")
 ap.add_argument("--lanes", default="0")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--peak", type=float, default=35.77)
+ap.add_argument("--flush", default="write", choices=("write", "write+read", "none"))
 a = ap.parse_args()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush2 = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+
+
+def do_flush():
+    if a.flush == "none":
+        return
+    flush.zero_()
+    if a.flush == "write+read":
+        flush2.max()      # clean lines displace the dirty ones (write-back outside timing)
 from paper_1811_01110_b200 import KernelSpec, TsConfig  # noqa: E402
 from paper_1811_01110_b200.kernels import Variant  # noqa: E402
 
@@ -44,7 +54,7 @@ for cs in a.cases.split(","):
             prob.evaluate()
         ts = []
         for _ in range(a.reps):
-            flush.zero_()
+            do_flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             prob.evaluate()
