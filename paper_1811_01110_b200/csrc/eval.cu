@@ -332,9 +332,6 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
 #ifndef TSQBX_RING
 #define TSQBX_RING 3
 #endif
-#ifndef TSQBX_PERSIST
-#define TSQBX_PERSIST 0
-#endif
 constexpr int kSellBlock = TSQBX_SELL_BLOCK;   // threads per CTA of the SELL kernels
 // minimum resident CTAs per SM requested from ptxas (caps registers per thread)
 #ifndef TSQBX_LAP_MINB
@@ -350,12 +347,6 @@ constexpr int kSellBlock = TSQBX_SELL_BLOCK;   // threads per CTA of the SELL ke
 #endif
 #ifndef TSQBX_HELM_MINB
 #define TSQBX_HELM_MINB 2
-#endif
-#ifndef TSQBX_LAP_UNROLL2
-#define TSQBX_LAP_UNROLL2 0
-#endif
-#ifndef TSQBX_HELM_CF_SMEM
-#define TSQBX_HELM_CF_SMEM 0
 #endif
 constexpr int kRing = TSQBX_RING;  // index blocks in flight (4 kRing entries of lookahead)
 constexpr int kSlots = kRing + 1;  // ring slots per thread (a power of two keeps b % kSlots a mask)
@@ -518,30 +509,12 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
         if (VAL) bm[q] = fmax(bm[q], B);
       }
     };
-#if TSQBX_LAP_UNROLL2
-    // two sources per trip: independent dependency chains for the scheduler; an
-    // odd tail pairs with a zero-weight dummy one unit away (finite, adds 0)
-    while (ss.more()) {
-      double4 qa, qb;
-      double wa, wb;
-      ss.next(qa, wa);
-      if (ss.more()) {
-        ss.next(qb, wb);
-      } else {
-        qb = make_double4(cx + 1.0, cy, cz, 0.0);
-        wb = 0.0;
-      }
-      source(qa, wa);
-      source(qb, wb);
-    }
-#else
     while (ss.more()) {
       double4 q4;
       double wim;
       ss.next(q4, wim);
       source(q4, wim);
     }
-#endif
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
@@ -559,8 +532,8 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
 template <int P, int NT, bool VAL>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[kSlots * kSellBlock];
-  const int64_t stride = TSQBX_PERSIST ? (int64_t)gridDim.x * blockDim.x : a.n_ctr;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ctr; g += stride) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < a.n_ctr) {
     const RowHead h = load_head(a, g);
     const bool realw = a.real_w || *a.imag_flag == 0u;
     if (realw)
@@ -572,19 +545,13 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_
 
 template <int P, int NT, bool VAL>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
-  // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n live in shared
-  // memory ([n][q][thread], conflict-free) instead of 2(P+1) registers per target
-#if TSQBX_HELM_CF_SMEM
-  __shared__ double cfs[(P + 1) * NT * kSellBlock];
-#define CF(n, q) cfs[((n) * NT + (q)) * kSellBlock + tid]
-#else
+  // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n, in registers
+  // (a shared-memory copy measured slower)
   double cfr[NT][P + 1];
 #define CF(n, q) cfr[q][n]
-#endif
   __shared__ int4 ring[kSlots * kSellBlock];
-  const int64_t stride = TSQBX_PERSIST ? (int64_t)gridDim.x * blockDim.x : a.n_ctr;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ctr; g += stride) {
-  const int tid = threadIdx.x;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < a.n_ctr) {
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
@@ -1444,25 +1411,13 @@ __global__ void pack_kernel(int64_t n, const double* __restrict__ xyz,
 // ---------------------------------------------------------------------------
 constexpr int kMaxFastOrder = 16;
 
-// CTAs of `kernel` (kSellBlock threads) resident at once on this device
-template <class K>
-int resident_blocks(K kernel) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSellBlock, 0);
-  return std::max(1, per_sm) * std::max(1, sms);
-}
-
 template <int P, int NT, bool VAL>
 void launch_fast(int equation, bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
   if (sell) {
-    int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
+    const int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
     if (equation == TSQBX_EQ_LAPLACE) {
-      if (TSQBX_PERSIST) blocks = std::min(blocks, resident_blocks(laplace_sell_kernel<P, NT, VAL>));
       laplace_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     } else {
-      if (TSQBX_PERSIST) blocks = std::min(blocks, resident_blocks(helmholtz_sell_kernel<P, NT, VAL>));
       helmholtz_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     }
     return;

@@ -5,16 +5,17 @@
 // tree lists, driver.py:197-228 / ilists.py:93-218; the closest analogue is
 // cKDTree.query_ball_point, costmodel.py:361-365).
 //
-// Pipeline (all stream-ordered, no host sync until the caller reads n_pairs):
-//   1. bounding box + max radius           (warp-reduced ordered-int atomics)
+// Pipeline (all stream-ordered; the caller reads the two totals once):
+//   1. bounding box + max radius           (block-reduced ordered-int atomics)
 //   2. fine Morton keys of sources/centers  (21 bits/axis; coarse cell = fine >> 3)
 //   3. CUB radix sort of both               -> src_perm, ctr_order ("tree leaf" order)
 //   4. open-addressed hash: coarse cell -> [start, end) in the sorted sources
-//   5. count: one warp per center; lanes look up the 27 neighbour cells, a
-//      warp bitonic sort puts them in Morton order, lanes sweep each cell,
-//      ballot + popc count members
-//   6. CUB exclusive scan -> near_ptr, n_pairs
-//   7. fill: same sweep, ballot-ranked stores -> rows ascending in sorted order
+//   5. count: one warp per 32 consecutive centers sweeps the union of their
+//      neighbour cells (or each distinct cell's 27 neighbours) through a
+//      shared-memory tile; per-lane member counts
+//   6. CUB exclusive scans -> near_ptr, SELL-32x4 slice offsets, totals
+//   7. fill: the same sweep; per-lane member bit masks, each lane appends its
+//      own members to its SELL column (16-byte stores); CSR entries on demand
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -260,132 +261,6 @@ __device__ __forceinline__ bool member(const double4 s, double cx, double cy, do
   const double dx = __dadd_rn(s.x, -cx), dy = __dadd_rn(s.y, -cy), dz = __dadd_rn(s.z, -cz);
   const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
   return d2 <= rad2;
-}
-
-// one warp per center (processing order); FILL = false counts, true writes
-template <bool FILL>
-__global__ void __launch_bounds__(256) sweep_kernel(
-    const double* __restrict__ ctr, const double* __restrict__ rad, int64_t n_ctr,
-    const int32_t* __restrict__ order, const double* __restrict__ prm,
-    const double4* __restrict__ sxyz, const unsigned long long* __restrict__ hkey,
-    const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
-    int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
-    const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
-  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (g >= n_ctr) return;
-  const int64_t ic = order[g];
-  const double cx = ctr[3 * ic], cy = ctr[3 * ic + 1], cz = ctr[3 * ic + 2];
-  const double r = rad[ic];
-  const double rad2 = __dmul_rn(r, r);
-  double pl[3] = {cx, cy, cz};
-  double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
-  unsigned long long f[3];
-  fine_coords(pl, prm_l, f);
-  const unsigned long long ccx = f[0] >> kSubBits, ccy = f[1] >> kSubBits, ccz = f[2] >> kSubBits;
-
-  unsigned long long key = kEmpty;
-  int st = 0, en = 0;
-  if (lane < 27) {
-    const unsigned long long nk =
-        morton3(ccx + (lane / 9) - 1, ccy + ((lane / 3) % 3) - 1, ccz + (lane % 3) - 1);
-    if (hash_find(hkey, hst, hen, cap, nk, st, en)) key = nk;
-  }
-  // warp bitonic sort of the neighbour cells by Morton key (ascending)
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, stride);
-      const int os = __shfl_xor_sync(0xffffffffu, st, stride);
-      const int oe = __shfl_xor_sync(0xffffffffu, en, stride);
-      const bool up = (lane & size) == 0 || size == 32;
-      const bool lower = (lane & stride) == 0;
-      const bool take = (lower == up) ? (ok < key) : (ok > key);
-      if (take) {
-        key = ok;
-        st = os;
-        en = oe;
-      }
-    }
-  }
-  int64_t count = 0;
-  const int64_t row0 = FILL ? nptr[g] : 0;
-  int64_t out = row0;
-  // SELL-32x4 slot of row entry i: sptr[g/32] + (i/4)*128 + (g%32)*4 + i%4
-  int32_t* sbase = (FILL && sidx) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
-  for (int L = 0; L < 27; ++L) {
-    const unsigned long long k = __shfl_sync(0xffffffffu, key, L);
-    if (k == kEmpty) break;
-    const int cs = __shfl_sync(0xffffffffu, st, L);
-    const int ce = __shfl_sync(0xffffffffu, en, L);
-    for (int base = cs; base < ce; base += 32) {
-      const int j = base + lane;
-      const bool m = j < ce && member(sxyz[j], cx, cy, cz, rad2);
-      const unsigned bal = __ballot_sync(0xffffffffu, m);
-      if (FILL && m) {
-        const int64_t at = out + __popc(bal & ((1u << lane) - 1u));
-        nidx[at] = j;
-        if (sbase) {
-          const int64_t i = at - row0;
-          sbase[(i >> 2) * 128 + (i & 3)] = j;
-        }
-      }
-      out += __popc(bal);
-      count += __popc(bal);
-    }
-  }
-  if (!FILL && lane == 0) cnt[g] = count;
-}
-
-// one THREAD per center (processing order): consecutive threads hold
-// Morton-adjacent centers, so their 27-cell neighbourhoods overlap and the
-// candidate loads hit L1.  Row order = cell enumeration (dz, dy, dx) order,
-// ascending within a cell.  FILL writes the CSR row and its SELL-32x4 column.
-template <bool FILL>
-__global__ void __launch_bounds__(128) sweep_thread_kernel(
-    const double* ctr, const double* rad, int64_t n_ctr,
-    const int32_t* order, const double* prm,
-    const double4* sxyz, const unsigned long long* hkey,
-    const int32_t* hst, const int32_t* hen, int64_t cap,
-    int64_t* cnt, const int64_t* nptr, int32_t* nidx,
-    const int64_t* sptr, int32_t* sidx) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_ctr) return;
-  const int64_t ic = order[g];
-  const double cx = ctr[3 * ic], cy = ctr[3 * ic + 1], cz = ctr[3 * ic + 2];
-  const double r = rad[ic];
-  const double rad2 = __dmul_rn(r, r);
-  const double pl[3] = {cx, cy, cz};
-  const double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
-  unsigned long long f[3];
-  fine_coords(pl, prm_l, f);
-  const unsigned long long ccx = f[0] >> kSubBits, ccy = f[1] >> kSubBits, ccz = f[2] >> kSubBits;
-  int32_t* row = FILL ? nidx + nptr[g] : nullptr;
-  int32_t* sbase = (FILL && sidx) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
-  int k = 0;
-  for (int dx = 0; dx < 3; ++dx) {
-   for (int dy = 0; dy < 3; ++dy) {
-    for (int dz = 0; dz < 3; ++dz) {
-    const unsigned long long key = morton3(ccx + dx - 1, ccy + dy - 1, ccz + dz - 1);
-    int st = 0, en = 0;
-    if (!hash_find(hkey, hst, hen, cap, key, st, en)) en = st;
-    for (int j = st; j < en; ++j) {
-      if (member(sxyz[j], cx, cy, cz, rad2)) {
-        if (FILL) {
-          row[k] = j;
-          if (sbase) sbase[(k >> 2) * 128 + (k & 3)] = j;
-        }
-        ++k;
-      }
-    }
-    }
-   }
-  }
-  if (!FILL) cnt[g] = k;
-#ifdef TSQBX_DEBUG_FILL
-  if (FILL && cnt && k != nptr[g + 1] - nptr[g]) atomicAdd((unsigned long long*)cnt, 1ull);
-#endif
 }
 
 // one WARP per 32 consecutive centers (processing order).  Consecutive centers
@@ -678,9 +553,6 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
   auto* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
   void* tmp = ws + L.off_tmp;
 
-#ifdef TSQBX_DEBUG_FILL
-  cudaMemsetAsync(workspace, 0, L.total, st);
-#endif
   init_bounds<<<1, 32, 0, st>>>(mm);
   if (n_src + n_ctr > 0) {
     int nb = (int)std::min<int64_t>((n_src + n_ctr + 255) / 256, 148 * 8);
@@ -744,11 +616,7 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
       reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
       reinterpret_cast<const int32_t*>(ws + L.off_hst),
       reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap,
-#ifdef TSQBX_DEBUG_FILL
-      reinterpret_cast<int64_t*>(ws + L.off_wid), near_ptr, near_idx,
-#else
       nullptr, near_ptr, near_idx,
-#endif
       sell_idx ? sell_ptr : nullptr, sell_idx);
   return check_cuda(cudaGetLastError(), "near_fill launch");
 }
