@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 5
+#define TSQBX_ABI_VERSION 6
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -149,17 +149,25 @@ int tsqbx_validate(const double* packed, int64_t n_src,
  * defines radius balls).  member(s, c) iff ((dx*dx + dy*dy) + dz*dz) <= rad*rad
  * in round-to-nearest without contraction.
  *
- * Two phases sharing one caller-owned workspace:
- *   tsqbx_near_count: Morton-sorts sources and centers, counts, scans.
- *       Writes src_perm (sorted position -> user source), ctr_order
- *       (processing position -> user center), near_ptr (n_ctr + 1, rows in
- *       processing order), optionally sell_ptr (SELL-32x4 slice offsets,
- *       ceil(n_ctr/32) + 1 entries) and totals[0] = n_pairs, totals[1] =
- *       SELL entries (device int64[2]; one read-back sizes both index arrays).
- *   tsqbx_near_fill : writes near_idx (n_pairs entries, indices into the
- *       sorted source order; may be NULL) and, when sell_idx is given, the
- *       same lists in the SELL-32x4 layout.  Row order: the 27 neighbour
- *       cells in (dx, dy, dz) order, ascending within a cell.
+ * Two phases sharing one caller-owned workspace.  Row order: processing
+ * (Morton) order of the centers; entries in the order of the 27 neighbour
+ * cells (dx, dy, dz), ascending within a cell.
+ *
+ * CSR mode (sell_ptr == NULL in count):
+ *   tsqbx_near_count: Morton-sorts sources and centers, counts the members of
+ *       every row exactly; writes src_perm (sorted position -> user source),
+ *       ctr_order (processing position -> user center), near_ptr (n_ctr + 1)
+ *       and totals[0] = n_pairs.
+ *   tsqbx_near_fill : writes near_idx (indices into the sorted source order).
+ * SELL mode (sell_ptr given to count, sell_idx to fill, near_idx NULL):
+ *   tsqbx_near_count: as above, but instead of counting it bounds every row by
+ *       its candidate count (no distance tests) and writes sell_ptr (SELL-32x4
+ *       slice offsets, ceil(n_ctr/32) + 1 entries) and totals[1] = SELL slots
+ *       (totals[0] = -1): one read-back sizes sell_idx.
+ *   tsqbx_near_fill : writes every row straight into its slice (slots past a
+ *       row's length are never read), then near_ptr and totals[0] = n_pairs.
+ *       The CSR entries, when needed, come from tsqbx_sell_to_csr.
+ * totals is a device int64[2].
  * ------------------------------------------------------------------------- */
 int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src);
 int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
@@ -170,8 +178,8 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
 int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                     const double* src_xyz, int64_t n_src,
                     void* workspace, int64_t ws_bytes,
-                    const int32_t* ctr_order, const int64_t* near_ptr,
-                    int32_t* near_idx, const int64_t* sell_ptr, int32_t* sell_idx,
+                    const int32_t* ctr_order, int64_t* near_ptr, int32_t* near_idx,
+                    const int64_t* sell_ptr, int32_t* sell_idx, int64_t* totals,
                     void* stream);
 
 /* Reorder centers and their targets into the processing order `ctr_order`

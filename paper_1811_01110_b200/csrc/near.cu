@@ -273,7 +273,11 @@ __device__ __forceinline__ bool member(const double4 s, double cx, double cy, do
 // a cell -- identical in the count and the fill pass.
 constexpr int kTile = 256;
 
-template <bool FILL>
+// MODE 0: count members per row; 1: fill (SELL column and/or CSR row, plus
+// the row length when `cnt` is given); 2: bound -- no distance tests, the
+// slice width (32 x the largest candidate count of its rows, a multiple of 4)
+// into `cnt[slice]`, so the fill can write before the exact lengths are known.
+template <int MODE>
 __global__ void __launch_bounds__(128) sweep_cell_kernel(
     const double* __restrict__ ctr, const double* __restrict__ rad, int64_t n_ctr,
     const int32_t* __restrict__ order, const double* __restrict__ prm,
@@ -281,6 +285,7 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
     const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
     int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
     const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
+  constexpr bool FILL = MODE == 1;
   __shared__ double4 tile[4][kTile];
   __shared__ int32_t tid_[4][kTile];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -310,6 +315,7 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
                                        : nullptr;
   int4 pend = make_int4(0, 0, 0, 0);   // entries of the current SELL block not yet stored
   int k = 0;
+  int64_t ub = 0;                      // MODE 2: candidates this row will test
   // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
   // c % 32, slot c / 32) through the tile; lanes with `mine` test them all.
   auto run_cells = [&](int ncell, int stA, int enA, int stB, int enB, bool mine) {
@@ -405,7 +411,13 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
         if (slot == 0) { stA = st; enA = en; } else { stB = st; enB = en; }
       }
     }
-    run_cells(ncell, stA, enA, stB, enB, valid);
+    if (MODE == 2) {
+      int64_t tot = (int64_t)(enA - stA) + (enB - stB);
+      for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+      ub = tot;
+    } else {
+      run_cells(ncell, stA, enA, stB, enB, valid);
+    }
   } else {
     // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
     const unsigned long long prev = __shfl_up_sync(0xffffffffu, ckey, 1);
@@ -419,11 +431,22 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
       const unsigned long long bz = __shfl_sync(0xffffffffu, ccz, a);
       int st = 0, en = 0;
       if (lane < 27) lookup(bx + (lane / 9) - 1, by + ((lane / 3) % 3) - 1, bz + (lane % 3) - 1, st, en);
-      run_cells(27, st, en, 0, 0, valid && ckey == cell);
+      if (MODE == 2) {
+        int64_t tot = en - st;
+        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+        if (valid && ckey == cell) ub = tot;
+      } else {
+        run_cells(27, st, en, 0, 0, valid && ckey == cell);
+      }
     }
   }
   if (FILL && sblk && (k & 3)) sblk[32 * (k >> 2)] = pend;     // partial last block
-  if (!FILL && valid) cnt[g] = k;
+  if (MODE == 0 && valid) cnt[g] = k;
+  if (MODE == 1 && valid && cnt) cnt[g] = k;
+  if (MODE == 2) {
+    for (int off = 16; off > 0; off >>= 1) ub = max(ub, __shfl_xor_sync(0xffffffffu, ub, off));
+    if (lane == 0 && (g >> 5) * 32 < n_ctr) cnt[g >> 5] = 32 * ((ub + 3) & ~3ll);
+  }
 }
 
 // CSR rows from the SELL-32x4 copy (thread per row; materialised on demand)
@@ -444,6 +467,7 @@ __global__ void sell_to_csr_kernel(const int64_t* __restrict__ nptr, int64_t n_r
 }
 
 __global__ void set_tail(int64_t* cnt, int64_t n) { cnt[n] = 0; }
+__global__ void set_key64(int64_t* p, int64_t v) { *p = v; }
 
 // one warp per 32-row slice: width = longest row; writes 32 * width (slice entries)
 __global__ void sell_width(const int64_t* __restrict__ nptr, int64_t n_rows,
@@ -574,50 +598,72 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     tb = L.tmp_bytes;
     cub::DeviceRadixSort::SortPairs(tmp, tb, ckey_in, ckey, cval_in, ctr_order, (int)n_ctr, 0,
                                     3 * kFineBits, st);
-    sweep_cell_kernel<false><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
-        ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, cnt, nullptr,
-        nullptr, nullptr, nullptr);
+    if (!sell_ptr)
+      sweep_cell_kernel<0><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+          ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, cnt, nullptr,
+          nullptr, nullptr, nullptr);
   }
-  set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
-  tb = L.tmp_bytes;
-  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
-  cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t),
-                                  cudaMemcpyDeviceToDevice, st);
-  if (e != cudaSuccess) return check_cuda(e, "near_count copy");
-  if (sell_ptr) {                       // SELL-32x4 offsets from the row lengths
+  cudaError_t e;
+  if (!sell_ptr) {                      // exact row lengths -> CSR offsets
+    set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
+    tb = L.tmp_bytes;
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
+    e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return check_cuda(e, "near_count copy");
+  } else {
+    // SELL-32x4 offsets from candidate-count bounds (no distance tests): the
+    // fill writes every row into its slice directly and produces the exact
+    // lengths (near_ptr, totals[0]) itself.  Slots past a row's length are
+    // never read.
     const int64_t n_sl = (n_ctr + 31) / 32;
     int64_t* wid = reinterpret_cast<int64_t*>(ws + L.off_wid);
-    if (n_sl > 0)
-      sell_width<<<(int)((n_sl * 32 + 255) / 256), 256, 0, st>>>(near_ptr, n_ctr, wid);
+    if (n_ctr > 0)
+      sweep_cell_kernel<2><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+          ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, wid, nullptr,
+          nullptr, nullptr, nullptr);
     sell_tail<<<1, 1, 0, st>>>(wid, n_sl);
     tb = L.tmp_bytes;
     cub::DeviceScan::ExclusiveSum(tmp, tb, wid, sell_ptr, (int)(n_sl + 1), st);
     e = cudaMemcpyAsync(totals + 1, sell_ptr + n_sl, sizeof(int64_t), cudaMemcpyDeviceToDevice,
                         st);
     if (e != cudaSuccess) return check_cuda(e, "near_count copy");
+    set_key64<<<1, 1, 0, st>>>(totals, -1);
   }
   return check_cuda(cudaGetLastError(), "near_count launch");
 }
 
 int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                     const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
-                    const int32_t* ctr_order, const int64_t* near_ptr, int32_t* near_idx,
-                    const int64_t* sell_ptr, int32_t* sell_idx, void* stream) {
+                    const int32_t* ctr_order, int64_t* near_ptr, int32_t* near_idx,
+                    const int64_t* sell_ptr, int32_t* sell_idx, int64_t* totals, void* stream) {
   (void)src_xyz;
   cudaStream_t st = (cudaStream_t)stream;
   const NearLayout L = near_layout(n_ctr, n_src);
   if (!workspace || ws_bytes < (int64_t)L.total)
     return set_error(TSQBX_ERR_ARGUMENT, "near_fill: workspace too small");
-  if (n_ctr == 0) return TSQBX_OK;
+  const bool sell = sell_idx != nullptr;
+  if (sell && (near_idx || !sell_ptr || !totals || !near_ptr))
+    return set_error(TSQBX_ERR_ARGUMENT,
+                     "near_fill: the SELL fill takes sell_ptr/sell_idx/near_ptr/totals and "
+                     "no CSR entries (derive them with tsqbx_sell_to_csr)");
   char* ws = static_cast<char*>(workspace);
-  sweep_cell_kernel<true><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
-      ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
-      reinterpret_cast<const double4*>(ws + L.off_sxyz),
-      reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
-      reinterpret_cast<const int32_t*>(ws + L.off_hst),
-      reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap,
-      nullptr, near_ptr, near_idx,
-      sell_idx ? sell_ptr : nullptr, sell_idx);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
+  if (n_ctr > 0)
+    sweep_cell_kernel<1><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+        ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
+        reinterpret_cast<const double4*>(ws + L.off_sxyz),
+        reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
+        reinterpret_cast<const int32_t*>(ws + L.off_hst),
+        reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, sell ? cnt : nullptr,
+        near_ptr, near_idx, sell ? sell_ptr : nullptr, sell_idx);
+  if (sell) {                           // exact lengths -> near_ptr, totals[0]
+    set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
+    size_t tb = L.tmp_bytes;
+    cub::DeviceScan::ExclusiveSum(ws + L.off_tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
+    const cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t),
+                                          cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return check_cuda(e, "near_fill copy");
+  }
   return check_cuda(cudaGetLastError(), "near_fill launch");
 }
 

@@ -155,14 +155,22 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
                                   ws.data_ptr(), ws_bytes, src_perm.data_ptr(),
                                   ctr_order.data_ptr(), nptr.data_ptr(), dv.ptr(sptr),
                                   totals.data_ptr(), st), "tsqbx_near_count")
-    n_pairs, n_sell = (int(v) for v in totals.cpu().tolist())
-    # with the SELL copy only it is written; the CSR entries are derived on demand
-    idx = None if sell else torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
-    sidx = torch.empty(max(n_sell, 4), dtype=torch.int32, device=dev) if sell else None
+    if sell:
+        # slice widths bounded by candidate counts: one read-back sizes the SELL
+        # slots, the fill then produces the exact row lengths
+        n_sell = int(totals[1].item())
+        idx = None
+        sidx = torch.empty(max(n_sell, 4), dtype=torch.int32, device=dev)
+    else:
+        n_pairs = int(totals[0].item())
+        idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
+        sidx = None
     _lib.check(L.tsqbx_near_fill(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
                                  ws.data_ptr(), ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
-                                 dv.ptr(idx), dv.ptr(sptr), dv.ptr(sidx), st),
+                                 dv.ptr(idx), dv.ptr(sptr), dv.ptr(sidx), totals.data_ptr(), st),
                "tsqbx_near_fill")
+    if sell:
+        n_pairs = int(totals[0].item())
     return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr,
                      csr_idx=None if idx is None else idx[:n_pairs],
                      src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],
