@@ -208,6 +208,12 @@ int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near
                     const int64_t* sell_ptr, int32_t* sell_idx, void* stream);
 
 /* CSR entries (near_idx, rows by near_ptr) from a SELL-32x4 copy. */
+/* Copy a SELL-32x4 layout into one with narrower slices (every slice of the
+ * destination no wider than the source's; e.g. the bound-sized build output into
+ * the exact widths of tsqbx_sell_size): a warp per slice copies its first
+ * (sell_ptr_dst[s+1] - sell_ptr_dst[s]) entries. */
+int tsqbx_sell_compact(int64_t n_rows, const int64_t* sell_ptr_src, const int32_t* sell_idx_src,
+                       const int64_t* sell_ptr_dst, int32_t* sell_idx_dst, void* stream);
 int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,
                       const int32_t* sell_idx, int32_t* near_idx, void* stream);
 

@@ -65,6 +65,7 @@ SIGNATURES = {
                                  _P]),
     "tsqbx_scatter_c128": (_I, [_I64, _P, _P, _P, _P]),
     "tsqbx_sell_to_csr": (_I, [_I64, _P, _P, _P, _P, _P]),
+    "tsqbx_sell_compact": (_I, [_I64, _P, _P, _P, _P, _P]),
     "tsqbx_sell_workspace_bytes": (_I64, [_I64]),
     "tsqbx_sell_size": (_I, [_I64, _P, _P, _I64, _P, _P, _P]),
     "tsqbx_sell_fill": (_I, [_I64, _P, _P, _P, _P, _P]),

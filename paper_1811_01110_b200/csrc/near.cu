@@ -466,6 +466,20 @@ __global__ void sell_to_csr_kernel(const int64_t* __restrict__ nptr, int64_t n_r
   }
 }
 
+// a warp per slice: the first dst-width blocks of a (wider) source slice
+__global__ void sell_compact_kernel(int64_t n_sl, const int64_t* __restrict__ sptr_src,
+                                    const int32_t* __restrict__ sidx_src,
+                                    const int64_t* __restrict__ sptr_dst,
+                                    int32_t* __restrict__ sidx_dst) {
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sl >= n_sl) return;
+  const int64_t n4 = (sptr_dst[sl + 1] - sptr_dst[sl]) >> 2;      // int4s to copy
+  const int4* src = reinterpret_cast<const int4*>(sidx_src + sptr_src[sl]);
+  int4* dst = reinterpret_cast<int4*>(sidx_dst + sptr_dst[sl]);
+  for (int64_t q = lane; q < n4; q += 32) dst[q] = src[q];
+}
+
 __global__ void set_tail(int64_t* cnt, int64_t n) { cnt[n] = 0; }
 __global__ void set_key64(int64_t* p, int64_t v) { *p = v; }
 
@@ -738,6 +752,18 @@ int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near
   sell_fill_kernel<<<(int)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       near_ptr, near_idx, n_rows, sell_ptr, sell_idx);
   return check_cuda(cudaGetLastError(), "sell_fill launch");
+}
+
+int tsqbx_sell_compact(int64_t n_rows, const int64_t* sell_ptr_src, const int32_t* sell_idx_src,
+                       const int64_t* sell_ptr_dst, int32_t* sell_idx_dst, void* stream) {
+  if (n_rows < 0 || (n_rows > 0 && (!sell_ptr_src || !sell_idx_src || !sell_ptr_dst ||
+                                    !sell_idx_dst)))
+    return set_error(TSQBX_ERR_ARGUMENT, "sell_compact: bad arguments");
+  const int64_t n_sl = (n_rows + 31) / 32;
+  if (n_sl == 0) return TSQBX_OK;
+  sell_compact_kernel<<<(unsigned)((n_sl * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      n_sl, sell_ptr_src, sell_idx_src, sell_ptr_dst, sell_idx_dst);
+  return check_cuda(cudaGetLastError(), "sell_compact launch");
 }
 
 int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,

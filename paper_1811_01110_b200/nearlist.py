@@ -123,6 +123,9 @@ class NearLists:
         return uptr, uidx.astype(np.int32)
 
 
+_BOUND_BYTES_MAX = 16 << 30     # bound-sized SELL buffer above this: count exactly
+
+
 def build_near_lists(centers, sources, radii, device=None, sell: bool = True) -> NearLists:
     """Radius-ball near lists {s : |s - c|^2 <= rad_c^2} on the device.
 
@@ -159,6 +162,21 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
         # slice widths bounded by candidate counts: one read-back sizes the SELL
         # slots, the fill then produces the exact row lengths
         n_sell = int(totals[1].item())
+        exact = n_sell * 4 > _BOUND_BYTES_MAX
+        if exact:
+            # a loose bound (radii far below the cell size, e.g. C5) would need
+            # too much memory: count exactly (the sorts run again), size the
+            # slices from the exact lengths and fill them directly
+            _lib.check(L.tsqbx_near_count(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
+                                          ws.data_ptr(), ws_bytes, src_perm.data_ptr(),
+                                          ctr_order.data_ptr(), nptr.data_ptr(), None,
+                                          totals.data_ptr(), st), "tsqbx_near_count")
+            wsb = int(L.tsqbx_sell_workspace_bytes(n_ctr))
+            sws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+            _lib.check(L.tsqbx_sell_size(n_ctr, nptr.data_ptr(), sws.data_ptr(), wsb,
+                                         sptr.data_ptr(), totals[1:].data_ptr(), st),
+                       "tsqbx_sell_size")
+            n_sell = int(totals[1].item())
         idx = None
         sidx = torch.empty(max(n_sell, 4), dtype=torch.int32, device=dev)
     else:
@@ -169,8 +187,23 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
                                  ws.data_ptr(), ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
                                  dv.ptr(idx), dv.ptr(sptr), dv.ptr(sidx), totals.data_ptr(), st),
                "tsqbx_near_fill")
-    if sell:
+    if sell and exact:
         n_pairs = int(totals[0].item())
+    elif sell:
+        n_pairs = int(totals[0].item())
+        # exact slice widths (the layout a counting build produces), then drop the
+        # bound-sized buffer
+        n_sl = (n_ctr + 31) // 32
+        wsb = int(L.tsqbx_sell_workspace_bytes(n_ctr))
+        sws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        xptr = torch.empty(n_sl + 1, dtype=torch.int64, device=dev)
+        _lib.check(L.tsqbx_sell_size(n_ctr, nptr.data_ptr(), sws.data_ptr(), wsb, xptr.data_ptr(),
+                                     totals[1:].data_ptr(), st), "tsqbx_sell_size")
+        n_exact = int(totals[1].item())
+        xidx = torch.empty(max(n_exact, 4), dtype=torch.int32, device=dev)
+        _lib.check(L.tsqbx_sell_compact(n_ctr, sptr.data_ptr(), sidx.data_ptr(), xptr.data_ptr(),
+                                        xidx.data_ptr(), st), "tsqbx_sell_compact")
+        sptr, sidx = xptr, xidx
     return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr,
                      csr_idx=None if idx is None else idx[:n_pairs],
                      src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],

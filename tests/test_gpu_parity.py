@@ -169,6 +169,29 @@ def test_near_lists_bit_exact(name, preset):
         assert np.array_equal(si[cells], d[p[g]:p[g + 1]])
 
 
+@pytest.mark.parametrize("mode", ["bound", "exact", "csr"])
+def test_near_list_build_paths_agree(mode, monkeypatch):
+    """The bound-sized SELL build (+ compaction), the exact-count fallback it
+    takes when the bound would be too large, and the CSR-only build give the
+    same rows, the same SELL layout, and the oracle's membership."""
+    from paper_1811_01110_b200 import nearlist
+    case = configs.make_case("c5", "literal", n=32768, spheres=4)
+    if mode == "exact":
+        monkeypatch.setattr(nearlist, "_BOUND_BYTES_MAX", 0)
+    near = build_near_lists(case.centers, case.sources, case.near_radii, sell=mode != "csr")
+    if mode == "csr":
+        near.build_sell()
+    ref = build_near_lists(case.centers, case.sources, case.near_radii)
+    assert torch.equal(near.ptr, ref.ptr)
+    assert torch.equal(near.sell_ptr, ref.sell_ptr)
+    assert torch.equal(near.idx, ref.idx)
+    uptr, uidx = near.to_user_csr()
+    optr, oidx = oracle.near_csr(case.centers, case.near_radii, case.sources)
+    assert np.array_equal(uptr, optr)
+    srt = np.concatenate([np.sort(uidx[uptr[i]:uptr[i + 1]]) for i in range(case.n_centers)])
+    assert np.array_equal(srt, oidx)
+
+
 def test_near_lists_repeated_builds_are_exact():
     """Alternating builds of different sizes reuse device memory; every build must
     reproduce the oracle membership exactly (guards against stale-memory and

@@ -17,5 +17,7 @@ for cs in cases:
         for _ in range(5):
             near = build_near_lists(c, s, r, sell=sell)
         torch.cuda.synchronize()
+        slots = int(near.sell_ptr[-1].item()) if sell else near.n_pairs
         print(f"{name}/{preset} sell={sell}: build {1e3 * (time.perf_counter() - t) / 5:.3f} ms, "
-              f"pairs {near.n_pairs}", flush=True)
+              f"pairs {near.n_pairs}, index slots {slots} ({slots / max(1, near.n_pairs):.2f}x)",
+              flush=True)
