@@ -319,12 +319,21 @@ def main_reference(args):
 def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
     """Device-resident kernel throughput for one case."""
     from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs
+    # device near-list build, steady state: geometry already in HBM, second build
+    # (the first one pays the allocator's cudaMalloc calls)
+    ctr_d = torch.as_tensor(case.centers, device=dev)
+    src_d = torch.as_tensor(case.sources, device=dev)
+    rad_d = torch.as_tensor(case.near_radii, device=dev)
+    near = build_near_lists(ctr_d, src_d, rad_d, dev)
+    del near
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
     e0.record()
-    near = build_near_lists(case.centers, case.sources, case.near_radii, dev)
+    near = build_near_lists(ctr_d, src_d, rad_d, dev)
     e1.record()
     torch.cuda.synchronize()
     csr_ms = e0.elapsed_time(e1)
+    del ctr_d, src_d, rad_d
     prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
                         tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev)
     pairs = prob.pair_count()

@@ -273,6 +273,39 @@ def test_c4_c5_full_size_one_percent(name, preset):
                  subset=max(4096, case.n_centers // 100))
 
 
+def test_c5_dense_full_size_one_percent():
+    """C5 dense at full size (8.39 M centers, 1.69 G pairs): a seeded 1 % subset
+    of the centers against the oracle; the subset's rows are cut out of the
+    device lists on the device (the full CSR is 6.7 GB)."""
+    case = configs.make_case("c5", "dense")
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr)
+    out = prob.evaluate(validate=True).cpu().numpy()
+    rng = np.random.default_rng(12)
+    sel = np.sort(rng.choice(case.n_centers, case.n_centers // 100, replace=False))
+    dev = near.ptr.device
+    row_of = torch.empty_like(near.ctr_order)
+    row_of[near.ctr_order.long()] = torch.arange(case.n_centers, dtype=row_of.dtype, device=dev)
+    rows = row_of[torch.as_tensor(sel, device=dev)].long()
+    b, e = near.ptr[rows], near.ptr[rows + 1]
+    lens = e - b
+    sptr = torch.zeros(len(sel) + 1, dtype=torch.int64, device=dev)
+    sptr[1:] = torch.cumsum(lens, 0)
+    pos = torch.arange(int(sptr[-1].item()), device=dev) - torch.repeat_interleave(sptr[:-1], lens)
+    ent = near.idx[torch.repeat_interleave(b, lens) + pos].long()
+    sidx = near.src_perm[ent].cpu().numpy().astype(np.int32)
+    sptr = sptr.cpu().numpy()
+    tl = np.diff(case.tgt_ptr)[sel]
+    tptr = np.concatenate([[0], np.cumsum(tl)])
+    tsel = np.concatenate([np.arange(case.tgt_ptr[c], case.tgt_ptr[c + 1]) for c in sel])
+    spec = case.cfg.spec
+    ref = oracle.ts_batch("helmholtz", 0, spec.helmholtz_k, case.cfg.p_qbx, case.sources,
+                          case.weights, case.centers[sel], sptr, sidx, case.targets[tsel], tptr)
+    assert sptr[-1] > 10_000_000
+    assert normwise(out[tsel], ref) <= HELM_TOL
+
+
 @pytest.mark.parametrize("name,preset", [("c1", "literal"), ("c1", "dense")])
 def test_c1_full(name, preset):
     _case_parity(configs.make_case(name, preset), LAP_TOL)
