@@ -97,6 +97,9 @@ int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const 
  *                 target t is written to out[(tgt_out ? tgt_out[t] : t) - out_offset]
  *   out         : complex128 potentials
  *   err_key     : device int64 (see above); may be NULL when flags lacks VALIDATE
+ *   group_lanes : CSR kernels: lanes per center (power of two <= 32, 0 = 8);
+ *                 SELL layout (Laplace S): threads per row, 1, 2 or 4 (a row
+ *                 split over lanes 32/S apart of one warp; 0 = 1)
  * A user CSR (rows by user center) is already in processing order (identity);
  * tsqbx_order_targets produces these arrays for a Morton order from
  * tsqbx_near_count.  A contiguous row range [g0, g1) of a problem is evaluated

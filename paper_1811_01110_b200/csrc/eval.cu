@@ -362,6 +362,7 @@ struct SellStream {
   const double4* __restrict__ sp;
   const double* __restrict__ swi;
   int4* ring;                     // [kRing + 1][kSellBlock] int4, this thread's column
+  int blk_stride = 32;            // int4s between this thread's consecutive blocks
   int count, nblk, i;
   int4 cur;                       // indices of the block being consumed / 4
   double4 q_next[D];
@@ -372,20 +373,26 @@ struct SellStream {
 
   __device__ __forceinline__ void issue(int b) {
     // block b goes to slot b % kSlots; always commit so group counts stay uniform
-    if (b < nblk) cp_async16(ring + (b % kSlots) * kSellBlock, blk + 32 * b);
+    if (b < nblk) cp_async16(ring + (b % kSlots) * kSellBlock, blk + blk_stride * b);
     cp_async_commit();
   }
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t g, int n, bool realw,
                                         int4* ring_base)
       : SellStream(a, a.sell_ptr[g >> 5], g, n, realw, ring_base, true) {}
   // `soff` = sell_ptr[g / 32], loaded by the caller; go = false only issues the
-  // first kRing index blocks (start() later waits for block 0 and gathers)
+  // first kRing index blocks (start() later waits for block 0 and gathers).
+  // b0 / bs: this thread takes the row's blocks b0, b0 + bs, ... (a row split
+  // over bs threads); `count` becomes the number of entries in those blocks.
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t soff, int64_t g, int n,
-                                        bool realw, int4* ring_base, bool go)
+                                        bool realw, int4* ring_base, bool go, int b0 = 0,
+                                        int bs = 1)
       : sp(a.sp), swi(a.swi), count(n), i(0), real_w(realw), snrm(a.snrm) {
-    blk = reinterpret_cast<const int4*>(a.sell_idx + soff) + (g & 31);
+    const int nb = (n + 3) >> 2;                       // blocks of the whole row
+    blk = reinterpret_cast<const int4*>(a.sell_idx + soff) + (g & 31) + 32 * b0;
+    blk_stride = 32 * bs;
     ring = ring_base + threadIdx.x;
-    nblk = (count + 3) >> 2;
+    nblk = nb > b0 ? (nb - b0 + bs - 1) / bs : 0;
+    count = nblk == 0 ? 0 : 4 * (nblk - 1) + min(4, n - 4 * (b0 + bs * (nblk - 1)));
     issue_first();
     if (go) start();
   }
@@ -465,9 +472,10 @@ __device__ __forceinline__ RowHead load_head(const EvalParams& a, int64_t g) {
   return h;
 }
 
-template <int P, int NT, bool VAL, bool REALW>
+template <int P, int NT, bool VAL, bool REALW, int S = 1>
 __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g,
-                                                  const RowHead& h, int4* ring) {
+                                                  const RowHead& h, int4* ring, int part = 0,
+                                                  unsigned gmask = 0xffffffffu) {
   const double cx = h.cx, cy = h.cy, cz = h.cz;
   const int len = h.len;
   const int64_t t0 = h.t0, t1 = h.t1;
@@ -475,7 +483,7 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
   // flight (measured: C4 dense p = 12 +7 %; p = 8 -2 %)
   using Stream = SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)>;
   // the index ring starts filling before the target range is known
-  Stream ss(a, h.soff, g, len, REALW, ring, false);
+  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S);
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
     int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
@@ -515,9 +523,22 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       ss.next(q4, wim);
       source(q4, wim);
     }
+    if (S > 1) {
+      // the S threads of this row hold partial sums over interleaved blocks:
+      // a fixed xor tree over the part bits (lanes 32/S apart) adds them
+#pragma unroll
+      for (int off = 32 / S; off < 32; off <<= 1) {
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          ar[q] += __shfl_xor_sync(gmask, ar[q], off);
+          if (!REALW) ai[q] += __shfl_xor_sync(gmask, ai[q], off);
+          if (VAL) bm[q] = fmax(bm[q], __shfl_xor_sync(gmask, bm[q], off));
+        }
+      }
+    }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      if (tb + q < t1) {
+      if (tb + q < t1 && part == 0) {
         a.out[slot[q]] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
         if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
           flag_suspect(a.err);
@@ -529,17 +550,30 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
 
 // real weights (the usual Laplace density) skip every Im w load and FMA; the
 // pack kernel records whether any Im w is nonzero, so no host round trip decides
-template <int P, int NT, bool VAL>
+//
+// S > 1 splits every row over S threads of one warp (lanes 32/S apart take
+// the row's SELL blocks round-robin; a CTA covers kSellBlock/S rows).  A
+// thread's row takes ~100 µs on the dense presets whatever else runs on its
+// SM (latency-bound per thread), so with whole rows the last partial wave of
+// rows leaves most slots idle; S rows-parts per row make the work units S
+// times shorter and the tail S times cheaper.
+template <int P, int NT, bool VAL, int S>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[kSlots * kSellBlock];
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int kRowsPerWarp = 32 / S;
+  const int lane = threadIdx.x & 31;
+  const int part = lane / kRowsPerWarp, rig = lane % kRowsPerWarp;
+  const int64_t g = (int64_t)blockIdx.x * (kSellBlock / S) + (threadIdx.x >> 5) * kRowsPerWarp + rig;
+  unsigned gmask = 0u;
+#pragma unroll
+  for (int k = 0; k < S; ++k) gmask |= 1u << (rig + k * kRowsPerWarp);
   if (g < a.n_ctr) {
     const RowHead h = load_head(a, g);
     const bool realw = a.real_w || *a.imag_flag == 0u;
     if (realw)
-      laplace_sell_body<P, NT, VAL, true>(a, g, h, ring);
+      laplace_sell_body<P, NT, VAL, true, S>(a, g, h, ring, part, gmask);
     else
-      laplace_sell_body<P, NT, VAL, false>(a, g, h, ring);
+      laplace_sell_body<P, NT, VAL, false, S>(a, g, h, ring, part, gmask);
   }
 }
 
@@ -1416,7 +1450,13 @@ void launch_fast(int equation, bool sell, const EvalParams& a, int64_t n_ctr, cu
   if (sell) {
     const int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
     if (equation == TSQBX_EQ_LAPLACE) {
-      laplace_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
+      // on the SELL layout `group_lanes` is the row split S (threads per row)
+      const int S = (a.G == 2 || a.G == 4) ? a.G : 1;
+      const int rows = kSellBlock / S;
+      const int lblocks = (int)((n_ctr + rows - 1) / rows);
+      if (S == 4) laplace_sell_kernel<P, NT, VAL, 4><<<lblocks, kSellBlock, 0, st>>>(a);
+      else if (S == 2) laplace_sell_kernel<P, NT, VAL, 2><<<lblocks, kSellBlock, 0, st>>>(a);
+      else laplace_sell_kernel<P, NT, VAL, 1><<<lblocks, kSellBlock, 0, st>>>(a);
     } else {
       helmholtz_sell_kernel<P, NT, VAL><<<blocks, kSellBlock, 0, st>>>(a);
     }

@@ -59,6 +59,20 @@ def pick_group_lanes(mean_len: float) -> int:
     return max(1, min(32, g))
 
 
+def pick_split(mean_len: float, n_rows: int, one_target: bool, sms: int = 148) -> int:
+    """Threads per row on the SELL layout (Laplace S): long rows are split over
+    2 threads of a warp (shorter work units: C2 dense +3.5 %, C4 dense +4 %),
+    over 4 when the rows do not fill one wave of the GPU (C1 dense 2.7x); short
+    rows (literal presets) are not split.  GIGAQBX_SPLIT overrides."""
+    env = os.environ.get("GIGAQBX_SPLIT")
+    if env:
+        return int(env)
+    if mean_len < 48:
+        return 1
+    waves = n_rows / (sms * (1024 if one_target else 768))
+    return 4 if waves < 1.0 else 2
+
+
 def pick_layout() -> str:
     """'sell' (thread per center on the sliced-ELL copy, the default) or 'csr'
     (groups of lanes per center on the CSR rows); GIGAQBX_LAYOUT overrides."""
@@ -121,8 +135,15 @@ class _Prepared:
                                                          self.n_tgt))
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
         self.err = torch.empty(1, dtype=torch.int64, device=dev)
-        self.G = int(group_lanes) if group_lanes else pick_group_lanes(near.mean_len)
         self.layout = "csr" if group_lanes else pick_layout()
+        if group_lanes:
+            self.G = int(group_lanes)
+        elif self.layout == "sell":
+            # on the SELL layout the ABI's group_lanes is the row split
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            self.G = pick_split(near.mean_len, self.n_ctr, self.n_tgt < 2 * self.n_ctr, sms)
+        else:
+            self.G = pick_group_lanes(near.mean_len)
         if self.layout == "sell" and self.n_ctr:
             near.build_sell()
         # real Laplace densities: the pack kernel flags any Im w != 0 on the device

@@ -393,6 +393,34 @@ def test_ragged_targets_and_empty_rows():
             assert np.all(out[tptr[ic]:tptr[ic + 1]] == 0)
 
 
+@pytest.mark.parametrize("split", ["1", "2", "4"])
+def test_row_split_matches_oracle(split, monkeypatch):
+    """Rows split over 1, 2 or 4 threads (SELL, Laplace S): ragged rows (0..70
+    entries, lengths not multiples of 4, rows shorter than the split), 0..3
+    targets per center, real and complex weights, validation on; and a dense
+    C2 subset."""
+    monkeypatch.setenv("GIGAQBX_SPLIT", split)
+    rng = np.random.default_rng(70 + int(split))
+    src = rng.normal(size=(500, 3)) * 0.5 + np.array([0, 0, 3.0])
+    n_ctr = 150
+    ctr = rng.normal(size=(n_ctr, 3)) * 0.1
+    ntg = rng.integers(0, 4, size=n_ctr)
+    tptr = np.concatenate([[0], np.cumsum(ntg)])
+    tgt = np.repeat(ctr, ntg, axis=0) + rng.normal(size=(tptr[-1], 3)) * 0.05
+    lens = rng.integers(0, 71, size=n_ctr)
+    lens[::7] = 0
+    lens[1::7] = 1
+    nptr = np.concatenate([[0], np.cumsum(lens)])
+    nidx = rng.integers(0, 500, size=nptr[-1]).astype(np.int32)
+    for w in (rng.uniform(0.5, 1.5, size=500) + 0j, rng.normal(size=500) + 1j * rng.normal(size=500)):
+        for p in (4, 8, 12):
+            out = ts_accumulate_batch(TsConfig(KernelSpec(), p), src, w, ctr, tgt, (nptr, nidx),
+                                      tgt_ptr=tptr)
+            ref = oracle.ts_batch("laplace", 0, 0.0, p, src, w, ctr, nptr, nidx, tgt, tptr)
+            assert normwise(out, ref) <= LAP_TOL
+    _case_parity(configs.make_case("c2", "dense", n=16384), LAP_TOL)
+
+
 def test_batch_validation_names_target_and_source():
     case = configs.make_case("c1", "literal", n=1024)
     tg = case.targets.copy()
