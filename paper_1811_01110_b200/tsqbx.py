@@ -139,9 +139,12 @@ class _Prepared:
         if group_lanes:
             self.G = int(group_lanes)
         elif self.layout == "sell":
-            # on the SELL layout the ABI's group_lanes is the row split
+            # on the SELL layout the ABI's group_lanes is the row split (Laplace S;
+            # splitting the Helmholtz rows measured 2 % slower: the per-target
+            # Bessel coefficients would be computed S times)
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            self.G = pick_split(near.mean_len, self.n_ctr, self.n_tgt < 2 * self.n_ctr, sms)
+            self.G = (pick_split(near.mean_len, self.n_ctr, self.n_tgt < 2 * self.n_ctr, sms)
+                      if spec.is_laplace and self.variant == 0 else 1)
         else:
             self.G = pick_group_lanes(near.mean_len)
         if self.layout == "sell" and self.n_ctr:
