@@ -1,0 +1,258 @@
+// eval_helmholtz.cu -- Helmholtz S kernels (compile-time order P <= 16): the
+// SELL-32x4 thread-per-row kernel and the CSR group kernel.
+#include "eval_kernels.cuh"
+
+namespace tsqbx {
+
+// ---------------------------------------------------------------------------
+// Helmholtz S, compile-time order P.  h_n(kR) is built once per source by the
+// upward recurrence (_core.pyx:190-193) and shared by the targets; each target
+// carries c_n = (2n+1) j_n(k|t-c|) kappa_n from the prologue table.
+// ---------------------------------------------------------------------------
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
+  GroupCoord gc;
+  if (!group_coord(a, gc)) return;
+  const int64_t g = gc.g;
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int64_t b = a.nptr[g];
+  const int len = (int)(a.nptr[g + 1] - b);
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
+
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT], cf[NT][P + 1];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      const double ux = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      const double uy = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      const double uz = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(uz, uz, fma(uy, uy, ux * ux));
+      const double ir = r2[q] > 0.0 ? rsqrt(r2[q]) : 0.0;  // r = 0: cos g irrelevant
+      tx[q] = ux * ir;
+      ty[q] = uy * ir;
+      tz[q] = uz * ir;
+#pragma unroll
+      for (int n = 0; n <= P; ++n)
+        cf[q][n] = ok ? a.ttab[(tb + q) * a.ttab_stride + n] : 0.0;
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    SourceStream ss = csr_stream(a, b, len, gc.lane, gc.G);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt_fast(R2);
+      const double x = k * (R2 * iR);
+      const double invx = iR * invk;
+      double hr[P + 1], hi[P + 1];
+      {
+        double h1r, h1i;
+        hankel01(k2 * R2, x, invx, hr[0], hi[0], h1r, h1i);
+        if constexpr (P >= 1) {
+          hr[1] = h1r;
+          hi[1] = h1i;
+        }
+      }
+#pragma unroll
+      for (int n = 1; n < P; ++n) {
+        const double f = (2.0 * n + 1.0) * invx;
+        hr[n + 1] = fma(f, hr[n], -hr[n - 1]);
+        hi[n + 1] = fma(f, hi[n], -hi[n - 1]);
+      }
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const double cg = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
+        double sr = cf[q][0] * hr[0], si = cf[q][0] * hi[0];
+        if constexpr (P >= 1) {
+          double pm = 1.0, pc = cg;
+          double c1 = cf[q][1] * pc;
+          sr = fma(c1, hr[1], sr);
+          si = fma(c1, hi[1], si);
+#pragma unroll
+          for (int n = 1; n < P; ++n) {
+            const double pn = fma(c_leg.alpha[n] * cg, pc, -pm);
+            pm = pc;
+            pc = pn;
+            const double cn = cf[q][n + 1] * pc;
+            sr = fma(cn, hr[n + 1], sr);
+            si = fma(cn, hi[n + 1], si);
+          }
+        }
+        ar[q] = fma(q4.w, sr, fma(-wim, si, ar[q]));
+        ai[q] = fma(q4.w, si, fma(wim, sr, ai[q]));
+        if (VAL) bm[q] = fmax(bm[q], r2[q] * (iR * iR));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      ar[q] = group_sum(ar[q], gc.G, gc.mask);
+      ai[q] = group_sum(ai[q], gc.G, gc.mask);
+      if (VAL) bm[q] = group_max(bm[q], gc.G, gc.mask);
+    }
+    if (gc.lane == 0) {
+      const double pk = k * kInvFourPi;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        if (tb + q < t1) {
+          a.out[out_slot(a, tb + q)] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
+          if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+            flag_suspect(a.err);
+        }
+      }
+    }
+  }
+}
+
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
+  // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n, in registers
+  // (a shared-memory copy measured slower)
+  double cfr[NT][P + 1];
+#define CF(n, q) cfr[q][n]
+  __shared__ int4 ring[kSlots * kSellBlock];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < a.n_ctr) {
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+    int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      slot[q] = ok ? out_slot(a, tb + q) : 0;
+      const double ux = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      const double uy = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      const double uz = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(uz, uz, fma(uy, uy, ux * ux));
+      const double ir = r2[q] > 0.0 ? rsqrt(r2[q]) : 0.0;  // r = 0: cos g irrelevant
+      tx[q] = ux * ir;
+      ty[q] = uy * ir;
+      tz[q] = uz * ir;
+      // c_n = (2n+1) j_n(k r) kappa_n computed here, in registers (no table pass);
+      // j_n(0) = delta_n0 (_core.pyx:357)
+      {
+        double jn[P + 1];
+        const double rr = r2[q] * ir;                 // |t - c|
+        if (ok && rr > 0.0) {
+          miller_j_reg<P + 1>(k * rr, jn);
+        } else {
+#pragma unroll
+          for (int n = 0; n <= P; ++n) jn[n] = n == 0 && ok ? 1.0 : 0.0;
+        }
+#pragma unroll
+        for (int n = 0; n <= P; ++n) CF(n, q) = (2.0 * n + 1.0) * jn[n] * c_leg.kappa[n];
+      }
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    SellStream<> ss(a, g, len, false, ring);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt_fast(R2);
+      const double invx = iR * invk;
+      double hmr, hmi, hcr, hci;                 // h_{n-1}, h_n
+      hankel01(k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
+      double cg[NT], pm[NT], pc[NT], sr[NT], si[NT];
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        cg[q] = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
+        const double c0 = CF(0, q);
+        sr[q] = c0 * hmr;
+        si[q] = c0 * hmi;
+        if constexpr (P >= 1) {
+          const double c1 = CF(1, q) * cg[q];
+          sr[q] = fma(c1, hcr, sr[q]);
+          si[q] = fma(c1, hci, si[q]);
+        }
+        pm[q] = 1.0;
+        pc[q] = cg[q];
+      }
+#pragma unroll
+      for (int n = 1; n < P; ++n) {
+        // h_{n+1} = (2n+1)/x h_n - h_{n-1}   (_core.pyx:192-193)
+        const double f = (2.0 * n + 1.0) * invx;
+        const double hnr = fma(f, hcr, -hmr), hni = fma(f, hci, -hmi);
+        hmr = hcr;
+        hmi = hci;
+        hcr = hnr;
+        hci = hni;
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          const double pn = fma(c_leg.alpha[n] * cg[q], pc[q], -pm[q]);
+          pm[q] = pc[q];
+          pc[q] = pn;
+          const double c = CF(n + 1, q) * pn;
+          sr[q] = fma(c, hnr, sr[q]);
+          si[q] = fma(c, hni, si[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        ar[q] = fma(q4.w, sr[q], fma(-wim, si[q], ar[q]));
+        ai[q] = fma(q4.w, si[q], fma(wim, sr[q], ai[q]));
+        if (VAL) bm[q] = fmax(bm[q], r2[q] * (iR * iR));
+      }
+    }
+    const double pk = k * kInvFourPi;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      if (tb + q < t1) {
+        a.out[slot[q]] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
+        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+          flag_suspect(a.err);
+      }
+    }
+  }
+}  // rows
+}
+#undef CF
+
+template <template <int> class F, int... Ps>
+struct OrderTable {
+  template <class... Args>
+  static bool run(int p, Args&&... args) {
+    bool done = false;
+    ((p == Ps ? (F<Ps>::go(args...), done = true) : false), ...);
+    return done;
+  }
+};
+
+template <int P>
+struct HelmholtzLaunch {
+  template <int NT, bool VAL>
+  static void one(bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
+    if (sell)
+      helmholtz_sell_kernel<P, NT, VAL>
+          <<<(int)((n_ctr + kSellBlock - 1) / kSellBlock), kSellBlock, 0, st>>>(a);
+    else
+      helmholtz_s_kernel<P, NT, VAL><<<(int)((n_ctr * a.G + 255) / 256), 256, 0, st>>>(a);
+  }
+  static void go(bool sell, int nt, bool val, const EvalParams& a, int64_t n_ctr,
+                 cudaStream_t st) {
+    if (nt >= 2) {
+      if (val) one<2, true>(sell, a, n_ctr, st);
+      else one<2, false>(sell, a, n_ctr, st);
+    } else {
+      if (val) one<1, true>(sell, a, n_ctr, st);
+      else one<1, false>(sell, a, n_ctr, st);
+    }
+  }
+};
+
+bool launch_helmholtz_fast(int p, bool sell, int nt, bool val, const EvalParams& a,
+                           int64_t n_ctr, cudaStream_t st) {
+  return OrderTable<HelmholtzLaunch, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15,
+                    16>::run(p, sell, nt, val, a, n_ctr, st);
+}
+
+}  // namespace tsqbx

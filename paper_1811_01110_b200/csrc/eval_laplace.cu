@@ -1,0 +1,221 @@
+// eval_laplace.cu -- Laplace S kernels (compile-time order P <= 16): the
+// SELL-32x4 thread-per-row kernel (the hot path) and the CSR group kernel.
+#include "eval_kernels.cuh"
+
+namespace tsqbx {
+
+// ---------------------------------------------------------------------------
+// Laplace S, compile-time order P, NT targets per pass.
+// Per pair: s-c, R^2, 1/R shared by the targets; per target A = (s-c).(t-c)/R^2,
+// B = |t-c|^2/R^2 and the 3-op/order Clenshaw series (common.cuh).
+// ---------------------------------------------------------------------------
+template <int P, int NT, bool VAL>
+__global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
+  GroupCoord gc;
+  if (!group_coord(a, gc)) return;
+  const int64_t g = gc.g;
+  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
+  const int64_t b = a.nptr[g];
+  const int len = (int)(a.nptr[g + 1] - b);
+  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      tx[q] = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    SourceStream ss = csr_stream(a, b, len, gc.lane, gc.G);
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt_fast(R2);
+      const double iR2 = iR * iR;
+      const double wr = q4.w * iR, wi = wim * iR;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const double A = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR2;
+        const double B = r2[q] * iR2;
+        const double S = laplace_series<P>(A, B);
+        ar[q] = fma(S, wr, ar[q]);
+        ai[q] = fma(S, wi, ai[q]);
+        if (VAL) bm[q] = fmax(bm[q], B);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      ar[q] = group_sum(ar[q], gc.G, gc.mask);
+      ai[q] = group_sum(ai[q], gc.G, gc.mask);
+      if (VAL) bm[q] = group_max(bm[q], gc.G, gc.mask);
+    }
+    if (gc.lane == 0) {
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        if (tb + q < t1) {
+          a.out[out_slot(a, tb + q)] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
+          if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+            flag_suspect(a.err);
+        }
+      }
+    }
+  }
+}
+
+template <int P, int NT, bool VAL, bool REALW, int S = 1>
+__device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g,
+                                                  const RowHead& h, int4* ring, int part = 0,
+                                                  unsigned gmask = 0xffffffffu) {
+  const double cx = h.cx, cy = h.cy, cz = h.cz;
+  const int len = h.len;
+  const int64_t t0 = h.t0, t1 = h.t1;
+  // high orders have more arithmetic per source to cover a second gather in
+  // flight (measured: C4 dense p = 12 +7 %; p = 8 -2 %)
+  using Stream = SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)>;
+  // the index ring starts filling before the target range is known
+  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S);
+  for (int64_t tb = t0; tb < t1; tb += NT) {
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+    int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const bool ok = tb + q < t1;
+      slot[q] = ok ? out_slot(a, tb + q) : 0;
+      tx[q] = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
+      ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
+      tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
+      r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
+      ar[q] = ai[q] = bm[q] = 0.0;
+    }
+    if (tb == t0) ss.start();
+    else ss.restart();
+    // one source against the NT targets
+    auto source = [&](const double4& q4, double wim) {
+      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
+      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double iR = rsqrt_fast(R2);
+      const double iR2 = iR * iR;
+      const double wr = q4.w * iR;
+      const double wi = REALW ? 0.0 : wim * iR;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const double A = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR2;
+        const double B = r2[q] * iR2;
+        const double ser = laplace_series<P>(A, B);
+        ar[q] = fma(ser, wr, ar[q]);
+        if (!REALW) ai[q] = fma(ser, wi, ai[q]);
+        if (VAL) bm[q] = fmax(bm[q], B);
+      }
+    };
+    while (ss.more()) {
+      double4 q4;
+      double wim;
+      ss.next(q4, wim);
+      source(q4, wim);
+    }
+    if (S > 1) {
+      // the S threads of this row hold partial sums over interleaved blocks:
+      // a fixed xor tree over the part bits (lanes 32/S apart) adds them
+#pragma unroll
+      for (int off = 32 / S; off < 32; off <<= 1) {
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          ar[q] += __shfl_xor_sync(gmask, ar[q], off);
+          if (!REALW) ai[q] += __shfl_xor_sync(gmask, ai[q], off);
+          if (VAL) bm[q] = fmax(bm[q], __shfl_xor_sync(gmask, bm[q], off));
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      if (tb + q < t1 && part == 0) {
+        a.out[slot[q]] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
+        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+          flag_suspect(a.err);
+      }
+    }
+  }
+  if (t0 >= t1) cp_async_wait<0>();   // no pass consumed the ring: drain it before exit
+}
+
+// real weights (the usual Laplace density) skip every Im w load and FMA; the
+// pack kernel records whether any Im w is nonzero, so no host round trip decides
+//
+// S > 1 splits every row over S threads of one warp (lanes 32/S apart take
+// the row's SELL blocks round-robin; a CTA covers kSellBlock/S rows).  A
+// thread's row takes ~100 µs on the dense presets whatever else runs on its
+// SM (latency-bound per thread), so with whole rows the last partial wave of
+// rows leaves most slots idle; S rows-parts per row make the work units S
+// times shorter and the tail S times cheaper.
+template <int P, int NT, bool VAL, int S>
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
+  __shared__ int4 ring[kSlots * kSellBlock];
+  constexpr int kRowsPerWarp = 32 / S;
+  const int lane = threadIdx.x & 31;
+  const int part = lane / kRowsPerWarp, rig = lane % kRowsPerWarp;
+  const int64_t g = (int64_t)blockIdx.x * (kSellBlock / S) + (threadIdx.x >> 5) * kRowsPerWarp + rig;
+  unsigned gmask = 0u;
+#pragma unroll
+  for (int k = 0; k < S; ++k) gmask |= 1u << (rig + k * kRowsPerWarp);
+  if (g < a.n_ctr) {
+    const RowHead h = load_head(a, g);
+    const bool realw = a.real_w || *a.imag_flag == 0u;
+    if (realw)
+      laplace_sell_body<P, NT, VAL, true, S>(a, g, h, ring, part, gmask);
+    else
+      laplace_sell_body<P, NT, VAL, false, S>(a, g, h, ring, part, gmask);
+  }
+}
+
+template <template <int> class F, int... Ps>
+struct OrderTable {
+  template <class... Args>
+  static bool run(int p, Args&&... args) {
+    bool done = false;
+    ((p == Ps ? (F<Ps>::go(args...), done = true) : false), ...);
+    return done;
+  }
+};
+
+template <int P>
+struct LaplaceLaunch {
+  template <int NT, bool VAL>
+  static void one(bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
+    if (sell) {
+      // on the SELL layout `group_lanes` is the row split S (threads per row)
+      const int S = (a.G == 2 || a.G == 4) ? a.G : 1;
+      const int rows = kSellBlock / S;
+      const int blocks = (int)((n_ctr + rows - 1) / rows);
+      if (S == 4) laplace_sell_kernel<P, NT, VAL, 4><<<blocks, kSellBlock, 0, st>>>(a);
+      else if (S == 2) laplace_sell_kernel<P, NT, VAL, 2><<<blocks, kSellBlock, 0, st>>>(a);
+      else laplace_sell_kernel<P, NT, VAL, 1><<<blocks, kSellBlock, 0, st>>>(a);
+      return;
+    }
+    laplace_s_kernel<P, NT, VAL><<<(int)((n_ctr * a.G + 255) / 256), 256, 0, st>>>(a);
+  }
+  static void go(bool sell, int nt, bool val, const EvalParams& a, int64_t n_ctr,
+                 cudaStream_t st) {
+    if (nt >= 2) {
+      if (val) one<2, true>(sell, a, n_ctr, st);
+      else one<2, false>(sell, a, n_ctr, st);
+    } else {
+      if (val) one<1, true>(sell, a, n_ctr, st);
+      else one<1, false>(sell, a, n_ctr, st);
+    }
+  }
+};
+
+bool launch_laplace_fast(int p, bool sell, int nt, bool val, const EvalParams& a, int64_t n_ctr,
+                         cudaStream_t st) {
+  return OrderTable<LaplaceLaunch, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::run(
+      p, sell, nt, val, a, n_ctr, st);
+}
+
+}  // namespace tsqbx
