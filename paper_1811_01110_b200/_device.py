@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 import torch
 
@@ -15,6 +17,12 @@ def require_cuda(device=None) -> torch.device:
     if dev.type != "cuda":
         raise RuntimeError(f"device {dev} is not a CUDA device")
     return dev
+
+
+@functools.lru_cache(maxsize=None)
+def sm_count(index: int) -> int:
+    """Multiprocessors of CUDA device ``index`` (cached: the query is not free)."""
+    return torch.cuda.get_device_properties(index).multi_processor_count
 
 
 def stream_handle(dev: torch.device) -> int:

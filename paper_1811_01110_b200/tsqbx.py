@@ -142,7 +142,7 @@ class _Prepared:
             # on the SELL layout the ABI's group_lanes is the row split (Laplace S;
             # splitting the Helmholtz rows measured 2 % slower: the per-target
             # Bessel coefficients would be computed S times)
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            sms = dv.sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
             self.G = (pick_split(near.mean_len, self.n_ctr, self.n_tgt < 2 * self.n_ctr, sms)
                       if spec.is_laplace and self.variant == 0 else 1)
         else:
