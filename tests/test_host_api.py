@@ -37,3 +37,13 @@ def test_kernelspec_validation():
         KernelSpec(helmholtz_k=1.0)
     with pytest.raises(ValueError, match="nonnegative"):
         TsConfig(KernelSpec(), -1)
+
+
+def test_row_split_choice(monkeypatch):
+    from paper_1811_01110_b200.tsqbx import pick_split
+    monkeypatch.delenv("GIGAQBX_SPLIT", raising=False)
+    assert pick_split(12.0, 262144, False) == 1          # literal rows: never split
+    assert pick_split(201.0, 262144, False) == 2         # dense, several waves
+    assert pick_split(201.0, 4096, True) == 4            # dense, under one wave
+    monkeypatch.setenv("GIGAQBX_SPLIT", "1")
+    assert pick_split(201.0, 262144, False) == 1
