@@ -15,7 +15,7 @@
 //      shared-memory tile; per-lane member counts
 //   6. CUB exclusive scans -> near_ptr, SELL-32x4 slice offsets, totals
 //   7. fill: the same sweep; per-lane member bit masks, each lane appends its
-//      own members to its SELL column (16-byte stores); CSR entries on demand
+//      own members to its SELL column (4-byte stores); CSR entries on demand
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
   // SELL-32x4 column of this row as int4 blocks: block b at sblk[32 b]
   int4* sblk = (FILL && valid && sidx) ? reinterpret_cast<int4*>(sidx + sptr[g >> 5]) + (g & 31)
                                        : nullptr;
-  int4 pend = make_int4(0, 0, 0, 0);   // entries of the current SELL block not yet stored
   int k = 0;
   int64_t ub = 0;                      // MODE 2: candidates this row will test
   // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
@@ -357,19 +356,13 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
           if (!FILL) {
             k += __popc(bits);
           } else {
+            int32_t* scol = reinterpret_cast<int32_t*>(sblk);
             while (bits) {
               const int u = __ffs(bits) - 1;
               bits &= bits - 1;
               const int j = tid_[wib][t0 + u];
               if (row) row[k] = j;
-              const int e = k & 3;
-              if (e == 0) pend.x = j;
-              else if (e == 1) pend.y = j;
-              else if (e == 2) pend.z = j;
-              else {
-                pend.w = j;
-                if (sblk) sblk[32 * (k >> 2)] = pend;   // one 16-byte store per 4 entries
-              }
+              if (scol) scol[128 * (k >> 2) + (k & 3)] = j;   // entry k of this row's column
               ++k;
             }
           }
@@ -440,7 +433,6 @@ __global__ void __launch_bounds__(128) sweep_cell_kernel(
       }
     }
   }
-  if (FILL && sblk && (k & 3)) sblk[32 * (k >> 2)] = pend;     // partial last block
   if (MODE == 0 && valid) cnt[g] = k;
   if (MODE == 1 && valid && cnt) cnt[g] = k;
   if (MODE == 2) {
