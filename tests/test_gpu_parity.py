@@ -520,3 +520,44 @@ def test_helmholtz_sin_cos_ranges(variant, band):
     ref = oracle.ts_batch("helmholtz", spec.variant_code, k, 10, src, w, ctr, nptr, nidx, tgt,
                           np.arange(n_ctr + 1, dtype=np.int64), snormals=sn, tnormals=tn)
     assert normwise(out, ref) <= HELM_TOL
+
+
+# --- convergence to the free-space kernel (test_tsqbx.py:93-99, 131-157) -------------
+def test_accumulate_single_equals_eval_times_weight():
+    rng = np.random.default_rng(4)
+    c = rng.normal(size=3)
+    s = c + 1.3 * rng.normal(size=3) / np.linalg.norm(rng.normal(size=3))
+    s = c + (s - c) / np.linalg.norm(s - c) * 1.1
+    t = c + 0.4 * (rng.normal(size=3) / np.linalg.norm(rng.normal(size=3)))
+    w = 1.3 - 0.4j
+    a = ts_accumulate(TsConfig(KernelSpec(), 8), s[None, :], np.array([w]), c, t)
+    b = w * ts_eval(TsConfig(KernelSpec(), 8), s, c, t)
+    assert a == pytest.approx(b, rel=1e-14)
+
+
+def test_laplace_convergence_order():
+    # fixed rho = r/R = 0.5: the truncation error decays like rho^{p+1}
+    from paper_1811_01110_b200 import direct_sum
+    c = np.zeros(3)
+    s = np.array([0.0, 0.8, 0.6])
+    t = 0.5 * np.array([0.6, -0.64, 0.48])
+    exact = direct_sum(KernelSpec(), s[None], [1.0], t[None])[0]
+    orders = np.arange(2, 16)
+    errs = [abs(ts_eval(TsConfig(KernelSpec(), int(p)), s, c, t) - exact) / abs(exact)
+            for p in orders]
+    slope = np.polyfit(orders + 1, np.log(errs), 1)[0]
+    assert abs(slope - math.log(0.5)) < 0.15 * abs(math.log(0.5))
+
+
+def test_helmholtz_convergence_trend():
+    # kR = 4: the error decreases monotonically with p towards the kernel value
+    from paper_1811_01110_b200 import direct_sum
+    spec = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=2.5)
+    c = np.zeros(3)
+    s = np.array([0.0, 0.0, 1.6])
+    t = np.array([0.4, 0.3, 0.0])
+    exact = direct_sum(spec, s[None], [1.0], t[None])[0]
+    errs = [abs(ts_eval(TsConfig(spec, p), s, c, t) - exact) / abs(exact)
+            for p in range(2, 20, 3)]
+    assert all(b < a for a, b in zip(errs, errs[1:]))
+    assert errs[-1] < 1e-8
