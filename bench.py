@@ -401,6 +401,33 @@ def measure_p2p(torch, dev, flush, peak, n=65536, reps=5):
     return res
 
 
+def measure_direct_stage(torch, dev, flush, reps=5):
+    """one driver direct stage (List 1) through DirectStage on a
+    synthetic C2-scale box structure (configs.synthetic_box_tree: 16r leaf cells,
+    65536 conventional targets at radius 1.02); plan cached as in a GMRES solve."""
+    from paper_1811_01110_b200 import KernelSpec, configs
+    from paper_1811_01110_b200.direct_stage import DirectStage
+    case = configs.make_case("c2", "literal")
+    rng = np.random.default_rng(1)
+    conv = rng.normal(size=(65536, 3))
+    conv = 1.02 * conv / np.linalg.norm(conv, axis=1)[:, None]
+    cell = 16 * float(case.expansion_radii.mean())
+    tree, lst, sp, cp, tboxes = configs.synthetic_box_tree(case, conv, cell)
+    qt = case.targets[case.tgt_ptr[:-1]][cp]
+    ds = DirectStage(KernelSpec(), 8, tree, tboxes, case.weights[sp], qtargets=qt, device=dev)
+    for _ in range(2):
+        _, _, nts = ds.run(lst)
+    ms = time_device_steps(torch, lambda: ds.run(lst), reps, flush)
+    mean = sum(ms) / len(ms)
+    ns = tree.owned_end[:, 0] - tree.owned_start[:, 0]
+    nt = tree.owned_end[:, 1] - tree.owned_start[:, 1]
+    per_box = np.add.reduceat(ns[lst.flat], lst.starts[:-1]) * (np.diff(lst.starts) > 0)
+    n_p2p = int((nt * per_box).sum())
+    return {"boxes": int(len(lst.starts) - 1), "ts_pairs": int(nts), "p2p_pairs": n_p2p,
+            "ms_per_stage": mean, "value": (nts + n_p2p) / (mean * 1e-3),
+            "unit": "pair-evals/s (TSQBX + p2p)"}
+
+
 def measure_e2e(torch, case, args, dev, with_near_lists=False):
     """Through the public API with host (pinned) buffers, every step: H2D of the
     step's inputs, TSQBX (validated), D2H of the potentials into a pinned buffer.
@@ -539,6 +566,7 @@ def main_ours(args):
             torch.cuda.empty_cache()
         line["secondary"] = sec
         line["p2p"] = measure_p2p(torch, dev, flush, peak)
+        line["direct_stage"] = measure_direct_stage(torch, dev, flush)
     print(json.dumps(line))
     return 0
 

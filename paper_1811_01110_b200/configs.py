@@ -165,3 +165,53 @@ def _spheres_case(n_per, count, preset, seed):
 def algorithmic_flops_per_pair(spec: KernelSpec, p: int) -> int:
     """Laplace S 7p + 17, Helmholtz S 14p + 30."""
     return 7 * p + 17 if spec.is_laplace else 14 * p + 30
+
+
+def synthetic_box_tree(case, conv, cell):
+    """A box structure for the driver's direct stages at BASELINE scale (row f2
+    measurements): leaf boxes = the occupied cells of a uniform grid of size
+    ``cell`` over the case's sources / centers and the conventional targets
+    ``conv``; List 1 of a box = its existing 27 neighbour cells.  Returns
+    (tree, list1, source order, center order, target boxes) duck-typed like the
+    reference's Octree / _Csr (points in tree order, owned ranges per box).
+    Not the reference's adaptive octree -- a stand-in of the same shape."""
+    from types import SimpleNamespace
+
+    lo = np.minimum(case.sources.min(0), conv.min(0)) - 1e-9
+    def cell_of(x):
+        return np.floor((x - lo) / cell).astype(np.int64)
+    dims = cell_of(np.maximum(case.sources.max(0), conv.max(0))) + 1
+    def key(c):
+        return (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
+    ks, kc, kt = key(cell_of(case.sources)), key(cell_of(case.centers)), key(cell_of(conv))
+    boxes = np.unique(np.concatenate([ks, kc, kt]))
+    nb = boxes.shape[0]
+
+    def order(keys):
+        perm = np.argsort(keys, kind="stable")
+        ids = np.searchsorted(boxes, keys[perm])
+        return perm, np.searchsorted(ids, np.arange(nb), "left"), \
+            np.searchsorted(ids, np.arange(nb), "right")
+    sp, s0, s1 = order(ks)
+    tp, t0, t1 = order(kt)
+    cp, c0, c1 = order(kc)
+    owned_start = np.stack([s0, t0, c0], 1)
+    owned_end = np.stack([s1, t1, c1], 1)
+    # List 1: the existing neighbour cells, in (dx, dy, dz) order
+    bx = np.stack([boxes // (dims[1] * dims[2]), (boxes // dims[2]) % dims[1], boxes % dims[2]], 1)
+    nbr = np.full((nb, 27), -1, np.int64)
+    for q, d in enumerate(np.ndindex(3, 3, 3)):
+        c = bx + np.array(d) - 1
+        ok = np.all((c >= 0) & (c < dims), axis=1)
+        kk = (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
+        j = np.searchsorted(boxes, kk)
+        j = np.minimum(j, nb - 1)
+        hit = ok & (boxes[j] == kk)
+        nbr[hit, q] = j[hit]
+    cnt = (nbr >= 0).sum(1)
+    starts = np.concatenate([[0], np.cumsum(cnt)])
+    flat = nbr[nbr >= 0]
+    tree = SimpleNamespace(points=[case.sources[sp], conv[tp], case.centers[cp]],
+                           owned_start=owned_start, owned_end=owned_end)
+    lst = SimpleNamespace(starts=starts.astype(np.int64), flat=flat.astype(np.int64))
+    return tree, lst, sp, cp, np.arange(nb)
