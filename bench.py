@@ -428,6 +428,11 @@ def measure_direct_stage(torch, dev, flush, reps=5):
             "unit": "pair-evals/s (TSQBX + p2p)"}
 
 
+def build_near_lists_for(case, dev):
+    from paper_1811_01110_b200 import build_near_lists
+    return build_near_lists(case.centers, case.sources, case.near_radii, dev)
+
+
 def measure_e2e(torch, case, args, dev, with_near_lists=False):
     """Through the public API with host (pinned) buffers, every step: H2D of the
     step's inputs, TSQBX (validated), D2H of the potentials into a pinned buffer.
@@ -534,6 +539,38 @@ def main_ours(args):
                                "reorder -> TSQBX (validated) -> D2H into a pinned buffer; "
                                "near lists pre-built on the device (as the reference's "
                                "ts_accumulate receives its near sources)"}
+        # a solver's matvec: geometry resident, a new density in each step
+        # (TsqbxProblem.set_weights: H2D of the weights, pack, evaluate, D2H)
+        from paper_1811_01110_b200 import TsqbxProblem
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        dens = [pin(case.weights * (1.0 + 0.1 * i)) for i in range(2)]
+        hout = torch.empty(case.n_targets, dtype=torch.complex128).pin_memory()
+        rprob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                             build_near_lists_for(case, dev), tgt_ptr=case.tgt_ptr, device=dev)
+
+        def matvec(i=[0]):  # noqa: B006
+            rprob.set_weights(dens[i[0] % 2])
+            i[0] += 1
+            hout.copy_(rprob.evaluate(validate=True))
+        for _ in range(3):
+            matvec()
+        torch.cuda.synchronize()
+        mms = []
+        for _ in range(max(1, args.steps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            matvec()
+            e1.record()
+            e1.synchronize()
+            mms.append(e0.elapsed_time(e1))
+        mm = sum(mms) / len(mms)
+        line["e2e_resident_geometry"] = {
+            "value": res["pairs_per_step"] / (mm * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": case.n_sources * 16, "d2h_bytes_per_step": case.n_targets * 16,
+            "ms_per_step": mm,
+            "path": "TsqbxProblem.set_weights(pinned density) -> evaluate (validated) -> D2H "
+                    "(GMRES matvec: geometry and near lists stay in HBM)"}
+        del rprob
         e2f = measure_e2e(torch, case, args, dev, with_near_lists=True)
         mean = sum(e2f["ms"]) / len(e2f["ms"])
         line["e2e_with_near_lists"] = {

@@ -561,3 +561,28 @@ def test_helmholtz_convergence_trend():
             for p in range(2, 20, 3)]
     assert all(b < a for a, b in zip(errs, errs[1:]))
     assert errs[-1] < 1e-8
+
+
+def test_helmholtz_small_k_matches_oracle():
+    # k -> 0: h_n(kR) and j_n(kr) at tiny arguments (Miller start p + 16 + ceil(kr))
+    case = configs.make_case("c3", "literal", n=4096)
+    spec = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=1e-6)
+    case.cfg = TsConfig(spec, 8)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    out = ts_accumulate_batch(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                              near, tgt_ptr=case.tgt_ptr)
+    uptr, uidx = near.to_user_csr()
+    ref = oracle.ts_batch("helmholtz", 0, 1e-6, 8, case.sources, case.weights, case.centers,
+                          uptr, uidx, case.targets, case.tgt_ptr)
+    assert normwise(out, ref) <= HELM_TOL
+
+
+def test_set_weights_reuses_the_problem():
+    case = configs.make_case("c2", "literal", n=8192)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr)
+    a = prob.evaluate().cpu().numpy().copy()
+    prob.set_weights(2.5 * case.weights)
+    b = prob.evaluate().cpu().numpy()
+    assert normwise(b, 2.5 * a) <= 1e-15
