@@ -30,24 +30,34 @@ class _OneCall:
         self.dev = dev
         self.cap = 0
         self.lock = threading.Lock()
+        # a private stream: the inputs come from the host and the call
+        # synchronises it, so no ordering with the caller's streams is needed,
+        # and its handle is looked up once instead of per call
+        self.stream = torch.cuda.Stream(dev)
+        self.stream_ptr = self.stream.cuda_stream
+        self.fn = _lib.load().tsqbx_eval_one
+        self.staging = _lib.load().tsqbx_one_staging_doubles
         self.res = torch.zeros(4, dtype=torch.float64).pin_memory()
         self.res_np = self.res.numpy()
+        self.res_ptr = self.res.data_ptr()
         self._grow(4096)
 
     def _grow(self, nd: int) -> None:
         cap = max(nd, 2 * self.cap)
         self.host = torch.zeros(cap, dtype=torch.float64).pin_memory()
         self.host_np = self.host.numpy()
+        self.host_ptr = self.host.data_ptr()
         self.devbuf = torch.empty(cap + 8, dtype=torch.float64, device=self.dev)
+        self.devbuf_ptr = self.devbuf.data_ptr()
+        self.devbuf_len = int(self.devbuf.numel())
         self.cap = cap
 
     def run(self, equation: int, variant: int, k: float, p: int, sources, weights, snormals,
             center, target, tnormal, validate: bool, r_ref: float = 0.0):
         """(value, key): key = _lib.ERR_KEY_NONE or (kind << 31) | position."""
-        L = _lib.load()
         n = sources.shape[0]
         with_nrm = variant == 2
-        nd = int(L.tsqbx_one_staging_doubles(n, int(with_nrm)))
+        nd = int(self.staging(n, int(with_nrm)))
         with self.lock:
             if nd > self.cap:
                 self._grow(nd)
@@ -68,12 +78,11 @@ class _OneCall:
                 sn = h[off:off + 4 * n].reshape(n, 4)
                 sn[:, :3] = snormals
                 sn[:, 3] = 0.0
-            _lib.check(L.tsqbx_eval_one(equation, variant, float(k), int(p),
-                                        self.host.data_ptr(), n,
-                                        _lib.FLAG_VALIDATE if validate else 0,
-                                        self.devbuf.data_ptr(), int(self.devbuf.numel()),
-                                        self.res.data_ptr(), dv.stream_handle(self.dev)),
-                       "tsqbx_eval_one")
+            rc = self.fn(equation, variant, float(k), int(p), self.host_ptr, n,
+                         _lib.FLAG_VALIDATE if validate else 0, self.devbuf_ptr,
+                         self.devbuf_len, self.res_ptr, self.stream_ptr)
+            if rc:
+                _lib.check(rc, "tsqbx_eval_one")
             value = complex(self.res_np[0], self.res_np[1])
             key = int(self.res_np[2:3].view(np.int64)[0])
         return value, key
@@ -81,10 +90,13 @@ class _OneCall:
 
 def one_call(equation: int, variant: int, k: float, p: int, sources, weights, snormals, center,
              target, tnormal, validate: bool = False, r_ref: float = 0.0):
-    dev = dv.require_cuda()
-    with _ctx_lock:
-        ctx = _ctx.get(dev)
-        if ctx is None:
-            ctx = _ctx[dev] = _OneCall(dev)
+    idx = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    ctx = _ctx.get(idx)
+    if ctx is None:
+        dev = dv.require_cuda()
+        with _ctx_lock:
+            ctx = _ctx.get(idx)
+            if ctx is None:
+                ctx = _ctx[idx] = _OneCall(dev)
     return ctx.run(equation, variant, k, p, sources, weights, snormals, center, target, tnormal,
                    validate, r_ref)
