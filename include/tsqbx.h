@@ -55,6 +55,9 @@ extern "C" {
 #define TSQBX_FLAG_REAL_WEIGHTS 4u /* caller guarantees Im w == 0: skip the imaginary part */
 #define TSQBX_FLAG_ONE_TARGET 8u   /* fast kernels: one target per pass (fewer registers) */
 #define TSQBX_FLAG_PRECISE 16u     /* p2p: IEEE 1/sqrt (after a non-finite screen with no singular pair) */
+/* eval: every row g owns targets [k g, k g + k) (tgt_ptr[g] == k g), k = (flags >> 8) & 0xff;
+ * the SELL kernels then address a row's targets without loading tgt_ptr */
+#define TSQBX_FLAG_UNIFORM_TARGETS 32u
 
 #define TSQBX_MAX_ORDER 64
 

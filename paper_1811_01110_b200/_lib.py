@@ -34,6 +34,7 @@ FLAG_GENERIC = 2
 FLAG_REAL_WEIGHTS = 4
 FLAG_ONE_TARGET = 8
 FLAG_PRECISE = 16
+FLAG_UNIFORM_TARGETS = 32
 MAX_ORDER = 64
 ERR_KEY_NONE = (1 << 63) - 1
 ERR_KEY_SUSPECT = (1 << 63) - 2

@@ -596,6 +596,11 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   a.sell_ptr = sell_ptr;
   a.sell_idx = sell_idx;
   a.real_w = (flags & TSQBX_FLAG_REAL_WEIGHTS) ? 1 : 0;
+  if (flags & TSQBX_FLAG_UNIFORM_TARGETS) {
+    a.tuni = (int)((flags >> 8) & 0xffu);
+    if (a.tuni < 1 || n_tgt != (int64_t)a.tuni * n_ctr)
+      return set_error(TSQBX_ERR_ARGUMENT, "uniform targets: n_tgt must be k * n_ctr, 1 <= k <= 255");
+  }
   a.tgt = tgt_xyz;
   a.tnrm = tgt_nrm;
   a.tptr = tgt_ptr;

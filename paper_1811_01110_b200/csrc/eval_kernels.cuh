@@ -33,6 +33,7 @@ struct EvalParams {
   int log2G;
   int validate;
   int real_w;                        // host assertion: all Im w == 0
+  int tuni;                          // k > 0: row g owns targets [k g, k g + k) (no tptr load)
   const unsigned* __restrict__ imag_flag;   // device: pack_kernel saw Im w != 0
   double k;
 };
@@ -260,12 +261,19 @@ struct RowHead {
   double cx, cy, cz;
   int len;
 };
+// UNI: row g owns targets [UNI g, UNI g + UNI) (TSQBX_FLAG_UNIFORM_TARGETS), no tptr load
+template <int UNI = 0>
 __device__ __forceinline__ RowHead load_head(const EvalParams& a, int64_t g) {
   RowHead h;
   h.soff = a.sell_ptr[g >> 5];
   h.len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  h.t0 = a.tptr[g];
-  h.t1 = a.tptr[g + 1];
+  if (UNI > 0) {       // uniform target runs: the target range needs no load
+    h.t0 = g * UNI;
+    h.t1 = h.t0 + UNI;
+  } else {
+    h.t0 = a.tptr[g];
+    h.t1 = a.tptr[g + 1];
+  }
   h.cx = a.ctr[3 * g];
   h.cy = a.ctr[3 * g + 1];
   h.cz = a.ctr[3 * g + 2];

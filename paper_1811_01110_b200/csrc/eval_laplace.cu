@@ -154,8 +154,46 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
 // SM (latency-bound per thread), so with whole rows the last partial wave of
 // rows leaves most slots idle; S rows-parts per row make the work units S
 // times shorter and the tail S times cheaper.
-template <int P, int NT, bool VAL, int S>
+#ifdef TSQBX_CTA_TIMING
+// debug builds only (tools/cta_timing_probe.py): per-CTA start/end globaltimer and SM id
+__device__ unsigned long long g_cta_t[2 * 8192];
+__device__ unsigned g_cta_sm[8192];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cta_mark_start() {
+  if (threadIdx.x == 0 && blockIdx.x < 8192) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_cta_t[2 * blockIdx.x] = gtimer();
+    g_cta_sm[blockIdx.x] = sm;
+  }
+}
+__device__ __forceinline__ void cta_mark_end() {
+  if (blockIdx.x < 8192) atomicMax(&g_cta_t[2 * blockIdx.x + 1], gtimer());
+}
+}  // namespace tsqbx
+extern "C" int tsqbx_debug_cta_times(unsigned long long* t, unsigned* sm, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(t, tsqbx::g_cta_t, sizeof(unsigned long long) * 2 * n);
+  cudaMemcpyFromSymbol(sm, tsqbx::g_cta_sm, sizeof(unsigned) * n);
+  static unsigned long long zero[2 * 8192];
+  cudaMemcpyToSymbol(tsqbx::g_cta_t, zero, sizeof(zero));
+  return 0;
+}
+namespace tsqbx {
+#define CTA_START() cta_mark_start()
+#define CTA_END() cta_mark_end()
+#else
+#define CTA_START()
+#define CTA_END()
+#endif
+
+template <int P, int NT, bool VAL, int S, int UNI>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
+  CTA_START();
   __shared__ int4 ring[kSlots * kSellBlock];
   constexpr int kRowsPerWarp = 32 / S;
   const int lane = threadIdx.x & 31;
@@ -165,13 +203,14 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_
 #pragma unroll
   for (int k = 0; k < S; ++k) gmask |= 1u << (rig + k * kRowsPerWarp);
   if (g < a.n_ctr) {
-    const RowHead h = load_head(a, g);
+    const RowHead h = load_head<UNI>(a, g);
     const bool realw = a.real_w || *a.imag_flag == 0u;
     if (realw)
       laplace_sell_body<P, NT, VAL, true, S>(a, g, h, ring, part, gmask);
     else
       laplace_sell_body<P, NT, VAL, false, S>(a, g, h, ring, part, gmask);
   }
+  CTA_END();
 }
 
 template <template <int> class F, int... Ps>
@@ -186,6 +225,12 @@ struct OrderTable {
 
 template <int P>
 struct LaplaceLaunch {
+  template <int NT, bool VAL, int UNI>
+  static void sell_launch(int S, int blocks, const EvalParams& a, cudaStream_t st) {
+    if (S == 4) laplace_sell_kernel<P, NT, VAL, 4, UNI><<<blocks, kSellBlock, 0, st>>>(a);
+    else if (S == 2) laplace_sell_kernel<P, NT, VAL, 2, UNI><<<blocks, kSellBlock, 0, st>>>(a);
+    else laplace_sell_kernel<P, NT, VAL, 1, UNI><<<blocks, kSellBlock, 0, st>>>(a);
+  }
   template <int NT, bool VAL>
   static void one(bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
     if (sell) {
@@ -193,9 +238,8 @@ struct LaplaceLaunch {
       const int S = (a.G == 2 || a.G == 4) ? a.G : 1;
       const int rows = kSellBlock / S;
       const int blocks = (int)((n_ctr + rows - 1) / rows);
-      if (S == 4) laplace_sell_kernel<P, NT, VAL, 4><<<blocks, kSellBlock, 0, st>>>(a);
-      else if (S == 2) laplace_sell_kernel<P, NT, VAL, 2><<<blocks, kSellBlock, 0, st>>>(a);
-      else laplace_sell_kernel<P, NT, VAL, 1><<<blocks, kSellBlock, 0, st>>>(a);
+      if (a.tuni == NT) sell_launch<NT, VAL, NT>(S, blocks, a, st);
+      else sell_launch<NT, VAL, 0>(S, blocks, a, st);
       return;
     }
     laplace_s_kernel<P, NT, VAL><<<(int)((n_ctr * a.G + 255) / 256), 256, 0, st>>>(a);

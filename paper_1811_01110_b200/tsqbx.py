@@ -153,6 +153,18 @@ class _Prepared:
         # and the kernel picks its real-weight path itself (no host round trip)
         self.real_w = False
         self.one_target = os.environ.get("GIGAQBX_ONE_TARGET", "0") == "1"
+        self.tuni = 0         # k > 0: every row owns k consecutive targets (set_uniform_targets)
+
+    def set_uniform_targets(self, known: bool = False) -> None:
+        """Let the SELL kernels address row g's targets as [k g, k g + k) instead of
+        loading tgt_ptr (one dependent load fewer per row).  ``known``: the caller
+        built tgt_ptr as arange * k; otherwise it is checked once on the device."""
+        k = self.n_tgt // self.n_ctr if self.n_ctr else 0
+        if not (1 <= k <= 255 and k * self.n_ctr == self.n_tgt):
+            return
+        if known or bool(torch.equal(self.tptr, torch.arange(
+                self.n_ctr + 1, dtype=torch.int64, device=self.dev) * k)):
+            self.tuni = k
 
     def pack(self, w: torch.Tensor) -> None:
         """(Re)pack the sources with weights ``w`` (interleaved float64 view)."""
@@ -176,6 +188,8 @@ class _Prepared:
                  | (_lib.FLAG_ONE_TARGET if self.one_target else 0))
         near = self.near
         g0, g1 = rows if rows is not None else (0, self.n_ctr)
+        if self.tuni and (g0, g1) == (0, self.n_ctr):
+            flags |= _lib.FLAG_UNIFORM_TARGETS | (self.tuni << 8)
         sell = self.layout == "sell" and near.sell_ptr is not None
         if sell and g0 % 32:
             raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
@@ -279,6 +293,8 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
         nptr, nidx = near
         near = NearLists.from_user_csr(nptr, nidx, int(src.shape[0]), dev)
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+    if tgt_ptr is None:
+        prep.set_uniform_targets(known=True)
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
         prep.launch(torch.view_as_real(res), validate)
@@ -324,6 +340,8 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
             else dv.to_device(tgt_ptr, torch.int64, dev))
     near = build_near_lists(ctr, src, rad, dev)
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+    if tgt_ptr is None:
+        prep.set_uniform_targets(known=True)
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
         prep.launch(torch.view_as_real(res), validate)
@@ -349,6 +367,7 @@ class TsqbxProblem:
         tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
                 else dv.to_device(tgt_ptr, torch.int64, dev))
         self.prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+        self.prep.set_uniform_targets(known=tgt_ptr is None)
         self.out = torch.empty(self.prep.n_tgt, dtype=torch.complex128, device=dev)
         self.n_pairs_per_target = None
 

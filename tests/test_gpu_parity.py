@@ -586,3 +586,26 @@ def test_set_weights_reuses_the_problem():
     prob.set_weights(2.5 * case.weights)
     b = prob.evaluate().cpu().numpy()
     assert normwise(b, 2.5 * a) <= 1e-15
+
+
+@pytest.mark.gpu
+def test_uniform_target_runs_flag():
+    """TSQBX_FLAG_UNIFORM_TARGETS (row g owns targets [k g, k g + k), no tgt_ptr
+    load) gives the same potentials as the tgt_ptr path; a ragged tgt_ptr is
+    detected and keeps the tgt_ptr path."""
+    case = configs.make_case("c2", "literal", n=4096)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                        near, tgt_ptr=case.tgt_ptr)
+    assert prob.prep.tuni == 2
+    fast = prob.evaluate(validate=True).cpu().numpy().copy()
+    prob.prep.tuni = 0
+    slow = prob.evaluate(validate=True).cpu().numpy()
+    assert np.array_equal(fast, slow)
+    ragged = case.tgt_ptr.copy()
+    ragged[1] -= 1                      # center 0 one target, center 1 three
+    rp = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
+                      tgt_ptr=ragged)
+    assert rp.prep.tuni == 0
+    one = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.sources, near)
+    assert one.prep.tuni == 1
