@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_se
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], rr[NT], ir[NT], nx[NT], ny[NT], nz[NT], ntt[NT];
-    double ar[NT], ai[NT], bm[NT];
+    double ar[NT], ai[NT];
+    long long rmin = 0x7ff0000000000000ll;   // min |s-c|^2 bits (see eval_laplace.cu)
     int64_t slot[NT];
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_se
         nz[q] = a.tnrm[3 * (tb + q) + 2];
         ntt[q] = fma(nz[q], tz[q], fma(ny[q], ty[q], nx[q] * tx[q])) * ir[q];  // nt . t^
       }
-      ar[q] = ai[q] = bm[q] = 0.0;
+      ar[q] = ai[q] = 0.0;
     }
     SellStream<VARIANT == 2> ss(a, g, len, realw, ring);
     while (ss.more()) {
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_se
       ss.next(q4, wim, n4);
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
       const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      if (val) rmin = min(rmin, __double_as_longlong(R2));
       const double iR = rsqrt_fast(R2);
       const double iR2 = iR * iR;
       const double wr = q4.w * iR2;
@@ -135,14 +137,13 @@ __global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_se
         }
         ar[q] = fma(sval, wr, ar[q]);
         ai[q] = fma(sval, wi, ai[q]);
-        if (val) bm[q] = fmax(bm[q], B);
       }
     }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
         a.out[slot[q]] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
-        if (val && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+        if (val && (!isfinite(ar[q]) || !isfinite(ai[q]) || r2[q] > kSepScreen * __longlong_as_double(rmin)))
           flag_suspect(a.err);
       }
     }
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], nx[NT], ny[NT], nz[NT], ntt[NT];
-    double ar[NT], ai[NT], bm[NT];
+    double ar[NT], ai[NT];
+    long long rmin = 0x7ff0000000000000ll;   // min |s-c|^2 bits (see eval_laplace.cu)
     int64_t slot[NT];
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
           CFA(n, q) = tw * jn[n];               // (D allocates only the first term)
         }
       }
-      ar[q] = ai[q] = bm[q] = 0.0;
+      ar[q] = ai[q] = 0.0;
     }
     SellStream<VARIANT == 2> ss(a, g, len, false, ring);
     while (ss.more()) {
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
       ss.next(q4, wim, n4);
       const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
       const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      if (val) rmin = min(rmin, __double_as_longlong(R2));
       const double iR = rsqrt_fast(R2);
       const double invx = iR * invk;
       double hmr, hmi, hcr, hci;                       // h_{n-1}, h_n, starting at n = 1
@@ -305,7 +308,6 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
         }
         ar[q] = fma(q4.w, sr, fma(-wim, si, ar[q]));
         ai[q] = fma(q4.w, si, fma(wim, sr, ai[q]));
-        if (val) bm[q] = fmax(bm[q], r2[q] * (iR * iR));
       }
     }
     const double pk = k * kInvFourPi;
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
         a.out[slot[q]] = make_double2(-ai[q] * pk, ar[q] * pk);
-        if (val && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+        if (val && (!isfinite(ar[q]) || !isfinite(ai[q]) || r2[q] > kSepScreen * __longlong_as_double(rmin)))
           flag_suspect(a.err);
       }
     }

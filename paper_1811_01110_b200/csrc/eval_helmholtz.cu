@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
   const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
-    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];
+    // VAL: min |s-c|^2 over the row as its IEEE bit pattern (R^2 >= 0, so the
+    // integer order is the numeric order): integer-pipe min, screen r^2 > R^2
+    long long rmin = 0x7ff0000000000000ll;
     int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
 #pragma unroll
         for (int n = 0; n <= P; ++n) CF(n, q) = (2.0 * n + 1.0) * jn[n] * c_leg.kappa[n];
       }
-      ar[q] = ai[q] = bm[q] = 0.0;
+      ar[q] = ai[q] = 0.0;
     }
     SellStream<> ss(a, g, len, false, ring);
     while (ss.more()) {
@@ -200,15 +203,15 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
       for (int q = 0; q < NT; ++q) {
         ar[q] = fma(q4.w, sr[q], fma(-wim, si[q], ar[q]));
         ai[q] = fma(q4.w, si[q], fma(wim, sr[q], ai[q]));
-        if (VAL) bm[q] = fmax(bm[q], r2[q] * (iR * iR));
       }
+      if (VAL) rmin = min(rmin, __double_as_longlong(R2));
     }
     const double pk = k * kInvFourPi;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1) {
         a.out[slot[q]] = make_double2(-ai[q] * pk, ar[q] * pk);  // (ik/4pi) acc
-        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || r2[q] > kSepScreen * __longlong_as_double(rmin)))
           flag_suspect(a.err);
       }
     }

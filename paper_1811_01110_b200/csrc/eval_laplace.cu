@@ -82,7 +82,10 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
   // the index ring starts filling before the target range is known
   Stream ss(a, h.soff, g, len, REALW, ring, false, part, S);
   for (int64_t tb = t0; tb < t1; tb += NT) {
-    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT], bm[NT];
+    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];
+    // VAL: min |s-c|^2 over the row as its IEEE bit pattern (R^2 >= 0, so the
+    // integer order is the numeric order): integer-pipe min, screen r^2 > R^2
+    long long rmin = 0x7ff0000000000000ll;
     int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
@@ -92,7 +95,7 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
       tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
       r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
-      ar[q] = ai[q] = bm[q] = 0.0;
+      ar[q] = ai[q] = 0.0;
     }
     if (tb == t0) ss.start();
     else ss.restart();
@@ -104,6 +107,7 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
       const double iR2 = iR * iR;
       const double wr = q4.w * iR;
       const double wi = REALW ? 0.0 : wim * iR;
+      if (VAL) rmin = min(rmin, __double_as_longlong(R2));
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         const double A = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR2;
@@ -111,7 +115,6 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
         const double ser = laplace_series<P>(A, B);
         ar[q] = fma(ser, wr, ar[q]);
         if (!REALW) ai[q] = fma(ser, wi, ai[q]);
-        if (VAL) bm[q] = fmax(bm[q], B);
       }
     };
     while (ss.more()) {
@@ -129,15 +132,15 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
         for (int q = 0; q < NT; ++q) {
           ar[q] += __shfl_xor_sync(gmask, ar[q], off);
           if (!REALW) ai[q] += __shfl_xor_sync(gmask, ai[q], off);
-          if (VAL) bm[q] = fmax(bm[q], __shfl_xor_sync(gmask, bm[q], off));
         }
+        if (VAL) rmin = min(rmin, __shfl_xor_sync(gmask, rmin, off));
       }
     }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       if (tb + q < t1 && part == 0) {
         a.out[slot[q]] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
-        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || bm[q] > kSepScreen))
+        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || r2[q] > kSepScreen * __longlong_as_double(rmin)))
           flag_suspect(a.err);
       }
     }
