@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
   int4* sblk = (FILL && valid && sidx) ? reinterpret_cast<int4*>(sidx + sptr[g >> 5]) + (g & 31)
                                        : nullptr;
   int k = 0;
+  int4 pend = make_int4(0, 0, 0, 0);   // fill, SELL only: the row's current block
   int64_t ub = 0;                      // MODE 2: candidates this row will test
   // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
   // c % 32, slot c / 32) through the tile; lanes with `mine` test them all.
@@ -357,6 +358,20 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
             if (u < m && member(tile[wib][t0 + u], cx, cy, cz, rad2)) bits |= 1u << u;
           if (!FILL) {
             k += __popc(bits);
+          } else if (!row) {
+            // SELL only: collect 4 members, then one 16-byte store of the block
+            while (bits) {
+              const int u = __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int j = tid_[wib][t0 + u];
+              const int e = k & 3;
+              pend.x = e == 0 ? j : pend.x;
+              pend.y = e == 1 ? j : pend.y;
+              pend.z = e == 2 ? j : pend.z;
+              pend.w = j;
+              if (e == 3 && sblk) sblk[32 * (k >> 2)] = pend;
+              ++k;
+            }
           } else {
             int32_t* scol = reinterpret_cast<int32_t*>(sblk);
             while (bits) {
@@ -435,6 +450,7 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
       }
     }
   }
+  if (FILL && !row && sblk && (k & 3)) sblk[32 * (k >> 2)] = pend;   // partial last block
   if (MODE == 0 && valid) cnt[g] = k;
   if (MODE == 1 && valid && cnt) cnt[g] = k;
   if (MODE == 2) {
