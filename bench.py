@@ -303,7 +303,7 @@ def main_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_seconds * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json configuration geometry)",
             "impl": "reference",
             "config": {"workload": workload_name(case), "case": case.name,
@@ -503,7 +503,7 @@ def main_ours(args):
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["mean_ms"],
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Fibonacci sphere etc., BASELINE.json geometry; inputs "
                 "resident in HBM for `value`)",
         "config": {"workload": workload_name(case), "case": case.name, "preset": case.preset,
