@@ -261,10 +261,50 @@ def _inputs(cfg, sources, weights, centers, targets, source_normals, target_norm
     return src, w, ctr, tgt, sn, tn
 
 
+class PendingPotentials:
+    """A ``ts_accumulate_batch(..., sync=False)`` evaluation in flight.
+
+    Everything -- the host-to-device copies, the kernels, the copy of the
+    potentials into a pinned host buffer and (with validation) of the error key
+    -- was enqueued on the stream that was current at the call, so evaluations
+    issued on two streams overlap one's PCIe transfers with the other's
+    arithmetic.  ``result()`` waits for this one, raises the reference's
+    ``ValueError`` if the screen flagged a pair, and returns the potentials."""
+
+    def __init__(self, prep, res: torch.Tensor, out, host_out: bool, validate: bool):
+        self._prep, self._res = prep, res
+        self._err = None
+        if validate and prep.n_tgt:
+            self._err = torch.empty(1, dtype=torch.int64, pin_memory=True)
+            self._err.copy_(prep.err, non_blocking=True)
+        self._numpy = out is None and host_out
+        if self._numpy:
+            out = torch.empty(res.shape, dtype=res.dtype, pin_memory=True)
+        if out is not None:
+            if not (isinstance(out, torch.Tensor) and out.device.type == "cpu"
+                    and out.is_pinned()):
+                raise ValueError("sync=False needs `out` to be a pinned host tensor (or None)")
+            out.copy_(res, non_blocking=True)
+        self._out = out
+        self._event = torch.cuda.Event()
+        self._event.record()
+
+    def done(self) -> bool:
+        return self._event.query()
+
+    def result(self):
+        self._event.synchronize()
+        if self._err is not None and int(self._err[0]) != _lib.ERR_KEY_NONE:
+            self._prep.check_errors(batch_context=True)
+        if self._out is None:
+            return self._res
+        return self._out.numpy() if self._numpy else self._out
+
+
 def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
                         tgt_ptr=None, source_normals=None, target_normals=None,
                         validate: bool = True, group_lanes: int | None = None, device=None,
-                        out=None):
+                        out=None, sync: bool = True):
     """Per-target TSQBX potentials for many centers in one launch.
 
     sources (n_src, 3), weights (n_src,) complex, centers (n_ctr, 3),
@@ -277,6 +317,10 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
     ``ts_accumulate(cfg, sources[near(c)], weights[near(c)], centers[c], t)``
     (tsqbx.py:68-80).  Returns complex128: numpy for host inputs, a CUDA
     tensor when ``sources`` is a CUDA tensor.
+
+    ``sync=False`` returns a :class:`PendingPotentials` instead: the whole call
+    is enqueued on the current stream (inputs should be pinned tensors, ``out``
+    a pinned tensor or None) and nothing waits for the GPU until ``result()``.
     """
     host_out = not (isinstance(sources, torch.Tensor) and sources.is_cuda)
     dev = dv.require_cuda(device)
@@ -298,8 +342,10 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
         prep.launch(torch.view_as_real(res), validate)
-        if validate:
-            prep.check_errors(batch_context=True)
+    if not sync:
+        return PendingPotentials(prep, res, out, host_out, validate)
+    if prep.n_tgt and validate:
+        prep.check_errors(batch_context=True)
     return _deliver(res, out, host_out)
 
 

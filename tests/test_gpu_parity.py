@@ -609,3 +609,37 @@ def test_uniform_target_runs_flag():
     assert rp.prep.tuni == 0
     one = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.sources, near)
     assert one.prep.tuni == 1
+
+
+@pytest.mark.gpu
+def test_async_batches_on_two_streams():
+    """ts_accumulate_batch(sync=False) on two streams (the overlapped e2e path):
+    same potentials as the synchronous call; the screen's ValueError surfaces at
+    result()."""
+    case = configs.make_case("c2", "literal", n=4096)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    args = (pin(case.sources), pin(case.weights), pin(case.centers), pin(case.targets), near)
+    ref = ts_accumulate_batch(case.cfg, *args, tgt_ptr=pin(case.tgt_ptr))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty(case.n_targets, dtype=torch.complex128).pin_memory() for _ in range(2)]
+    pend = []
+    for i in range(4):
+        with torch.cuda.stream(streams[i % 2]):
+            if len(pend) >= 2:
+                got = pend.pop(0).result()
+                assert np.array_equal(got.numpy(), ref)
+            pend.append(ts_accumulate_batch(case.cfg, *args, tgt_ptr=pin(case.tgt_ptr),
+                                            out=outs[i % 2], sync=False))
+    for p in pend:
+        assert np.array_equal(p.result().numpy(), ref)
+    # numpy result when no `out` is given
+    p = ts_accumulate_batch(case.cfg, *args, tgt_ptr=pin(case.tgt_ptr), sync=False)
+    assert np.array_equal(p.result(), ref)
+    # a separation violation is reported by result()
+    src = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 0.2]])
+    w = np.ones(2, complex)
+    p = ts_accumulate_batch(case.cfg, src, w, np.zeros((1, 3)), np.array([[0.0, 0.0, 0.5]]),
+                            (np.array([0, 2]), np.array([0, 1], np.int32)), sync=False)
+    with pytest.raises(ValueError, match="separation violation for source 1"):
+        p.result()
