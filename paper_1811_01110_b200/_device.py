@@ -25,6 +25,16 @@ def sm_count(index: int) -> int:
     return torch.cuda.get_device_properties(index).multi_processor_count
 
 
+@functools.lru_cache(maxsize=None)
+def _side_stream(index: int) -> torch.cuda.Stream:
+    return torch.cuda.Stream(torch.device("cuda", index))
+
+
+def side_stream(dev: torch.device) -> torch.cuda.Stream:
+    """A second stream per device for copies that overlap work on the current one."""
+    return _side_stream(dev.index if dev.index is not None else torch.cuda.current_device())
+
+
 def stream_handle(dev: torch.device) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 

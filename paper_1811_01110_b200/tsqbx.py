@@ -376,15 +376,28 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
 
     host_out = not (isinstance(sources, torch.Tensor) and sources.is_cuda)
     dev = dv.require_cuda(device)
-    src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, centers, targets, source_normals,
-                                       target_normals, dev)
+    # the geometry the near lists need goes first, on the current stream; the
+    # rest of the payload (weights, targets, offsets, normals) is copied on a
+    # side stream while the lists are built
+    src = dv.to_device(sources, torch.float64, dev, (-1, 3))
+    ctr = dv.to_device(centers, torch.float64, dev, (-1, 3))
     n_ctr = int(ctr.shape[0])
     rad = (near_radii.to(device=dev, dtype=torch.float64) if isinstance(near_radii, torch.Tensor)
            else dv.to_device(np.broadcast_to(np.asarray(near_radii, np.float64), (n_ctr,)),
                              torch.float64, dev))
-    tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
-            else dv.to_device(tgt_ptr, torch.int64, dev))
+    main = torch.cuda.current_stream(dev)
+    side = dv.side_stream(dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        _, w, _, tgt, sn, tn = _inputs(cfg, src, weights, ctr, targets, source_normals,
+                                       target_normals, dev)
+        tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
+                else dv.to_device(tgt_ptr, torch.int64, dev))
     near = build_near_lists(ctr, src, rad, dev)
+    main.wait_stream(side)
+    for t in (w, tgt, sn, tn, tptr):
+        if t is not None:
+            t.record_stream(main)
     prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
     if tgt_ptr is None:
         prep.set_uniform_targets(known=True)

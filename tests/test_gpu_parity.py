@@ -643,3 +643,23 @@ def test_async_batches_on_two_streams():
                             (np.array([0, 2]), np.array([0, 1], np.int32)), sync=False)
     with pytest.raises(ValueError, match="separation violation for source 1"):
         p.result()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pinned", [False, True])
+def test_near_field_potentials_matches_oracle(pinned):
+    """geometry -> device near lists -> potentials in one call (payload copied on a
+    side stream while the lists are built) equals the oracle on the oracle's lists."""
+    from paper_1811_01110_b200.tsqbx import near_field_potentials
+    case = configs.make_case("c3", "literal", n=4096)
+    conv = ((lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()) if pinned
+            else (lambda a: a))
+    got = near_field_potentials(case.cfg, conv(case.sources), conv(case.weights),
+                                conv(case.centers), conv(case.near_radii), conv(case.targets),
+                                tgt_ptr=conv(case.tgt_ptr))
+    got = got.numpy() if isinstance(got, torch.Tensor) else got
+    ptr, idx = oracle.near_csr(case.centers, case.near_radii, case.sources)
+    ref = oracle.ts_batch("helmholtz", 0, case.cfg.spec.helmholtz_k, case.cfg.p_qbx,
+                          case.sources, case.weights, case.centers, ptr, idx, case.targets,
+                          case.tgt_ptr)
+    assert normwise(got, ref) <= HELM_TOL
