@@ -190,16 +190,15 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
     if sell and exact:
         n_pairs = int(totals[0].item())
     elif sell:
-        n_pairs = int(totals[0].item())
         # exact slice widths (the layout a counting build produces), then drop the
-        # bound-sized buffer
+        # bound-sized buffer; one read-back gives the pair count and the slot count
         n_sl = (n_ctr + 31) // 32
         wsb = int(L.tsqbx_sell_workspace_bytes(n_ctr))
         sws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
         xptr = torch.empty(n_sl + 1, dtype=torch.int64, device=dev)
         _lib.check(L.tsqbx_sell_size(n_ctr, nptr.data_ptr(), sws.data_ptr(), wsb, xptr.data_ptr(),
                                      totals[1:].data_ptr(), st), "tsqbx_sell_size")
-        n_exact = int(totals[1].item())
+        n_pairs, n_exact = (int(v) for v in totals.tolist())
         xidx = torch.empty(max(n_exact, 4), dtype=torch.int32, device=dev)
         _lib.check(L.tsqbx_sell_compact(n_ctr, sptr.data_ptr(), sidx.data_ptr(), xptr.data_ptr(),
                                         xidx.data_ptr(), st), "tsqbx_sell_compact")
