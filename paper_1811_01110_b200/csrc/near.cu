@@ -25,7 +25,21 @@ namespace {
 
 constexpr unsigned long long kEmpty = ~0ull;
 constexpr int kFineBits = 21;
-constexpr int kSubBits = 3;  // coarse cell = 8 fine cells per axis
+constexpr int kSubBits = 3;  // level-0 coarse cell = 8 fine cells per axis
+// Cell levels: a center of radius r searches the 27 neighbours of its cell at
+// the smallest level L whose cell (8 fine cells << L) is >= r.  The fine grid
+// follows the smallest radius (down to rmax / 2^(kLevels-1)), so centers with
+// small radii no longer scan cells sized for the largest (C5's 16 spheres of
+// different radii, C4's per-source radii).  Level L cells are prefixes of the
+// fine Morton keys, so one source sort serves every level; the hash key of a
+// level-L cell carries L in bits 60-61.
+constexpr int kLevels = 4;
+// Levels multiply the hash entries; past ~1 M sources the table no longer
+// stays in L2 and the extra inserts and lookups cost more than the candidate
+// tests they save (C5 literal, 8.4 M sources: 10.8 ms one level, 12.3 ms four;
+// C4 literal, 1 M sources: 1.87 ms one level, 1.53 ms four).
+constexpr int64_t kMultiLevelMaxSources = 1 << 20;
+constexpr int kFineOffset = 1 << (kSubBits + kLevels - 1);  // coarse coordinate >= 1 at every level
 
 struct NearLayout {
   size_t off_mm, off_prm, off_skey_in, off_skey, off_sval_in, off_ckey_in, off_ckey, off_cval_in,
@@ -39,7 +53,9 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 NearLayout near_layout(int64_t n_ctr, int64_t n_src) {
   NearLayout L{};
   int64_t cap = 1024;
-  while (cap < 2 * n_src) cap <<= 1;
+  // room for the cells of every level while the table stays L2-resident
+  const int64_t factor = n_src <= kMultiLevelMaxSources ? 4 : 2;
+  while (cap < factor * n_src) cap <<= 1;
   L.cap = cap;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -114,6 +130,7 @@ __global__ void init_bounds(long long* mm) {
   if (i < 3) mm[i] = LLONG_MAX;                 // min x, y, z
   else if (i < 6) mm[i] = LLONG_MIN;            // max x, y, z
   else if (i == 6) mm[i] = LLONG_MIN;           // max radius
+  else if (i == 7) mm[i] = LLONG_MAX;           // min radius
 }
 
 __global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
@@ -121,7 +138,7 @@ __global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
                               int64_t n_ctr, long long* mm) {
   long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
   long long hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
-  long long rm = LLONG_MIN;
+  long long rm = LLONG_MIN, rn = LLONG_MAX;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_src + n_ctr;
        i += stride) {
@@ -132,7 +149,11 @@ __global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
       lo[d] = min(lo[d], o);
       hi[d] = max(hi[d], o);
     }
-    if (i >= n_src) rm = max(rm, ord_of(rad[i - n_src]));
+    if (i >= n_src) {
+      const long long o = ord_of(rad[i - n_src]);
+      rm = max(rm, o);
+      rn = min(rn, o);
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -142,9 +163,10 @@ __global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
       hi[d] = max(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], off));
     }
     rm = max(rm, __shfl_xor_sync(0xffffffffu, rm, off));
+    rn = min(rn, __shfl_xor_sync(0xffffffffu, rn, off));
   }
   // block reduction through shared memory, then one atomic per value per block
-  __shared__ long long red[7][32];
+  __shared__ long long red[8][32];
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
@@ -153,34 +175,53 @@ __global__ void bounds_kernel(const double* __restrict__ src, int64_t n_src,
       red[3 + d][w] = hi[d];
     }
     red[6][w] = rm;
+    red[7][w] = rn;
   }
   __syncthreads();
-  if (threadIdx.x < 7) {
+  if (threadIdx.x < 8) {
     const int v = threadIdx.x;
+    const bool is_min = v < 3 || v == 7;
     long long acc = red[v][0];
-    for (int q = 1; q < nw; ++q) acc = v < 3 ? min(acc, red[v][q]) : max(acc, red[v][q]);
-    if (v < 3) atomicMin(&mm[v], acc);
+    for (int q = 1; q < nw; ++q) acc = is_min ? min(acc, red[v][q]) : max(acc, red[v][q]);
+    if (is_min) atomicMin(&mm[v], acc);
     else atomicMax(&mm[v], acc);
   }
 }
 
-// prm = {lo_x, lo_y, lo_z, fine cell}
-__global__ void grid_params(const long long* mm, double* prm) {
+// prm = {lo_x, lo_y, lo_z, fine cell, top level}
+__global__ void grid_params(const long long* mm, double* prm, int levels) {
   double lo[3], ext = 0.0;
   for (int d = 0; d < 3; ++d) {
     lo[d] = of_ord(mm[d]);
     ext = fmax(ext, of_ord(mm[3 + d]) - lo[d]);
   }
   const double rmax = mm[6] == LLONG_MIN ? 0.0 : of_ord(mm[6]);
-  // coarse cell >= rmax (with slack for rounding of the cell index) so the
-  // 27 neighbours of a center's cell cover its ball; 2^21 fine cells per axis max
-  double fine = fmax(rmax * (1.0 + 1e-9) / (1 << kSubBits),
-                     ext / (double)((1 << kFineBits) - 32));
+  const double rmin = mm[7] == LLONG_MAX ? 0.0 : of_ord(mm[7]);
+  // level-0 cell >= the smallest radius (with slack for rounding of the cell
+  // index), but no finer than the top level needs to reach rmax; 2^21 fine
+  // cells per axis max
+  const double rlo = fmax(fmax(rmin, 0.0), rmax / (double)(1 << (levels - 1)));
+  double fine = fmax(rlo * (1.0 + 1e-9) / (1 << kSubBits),
+                     ext / (double)((1 << kFineBits) - 4 * kFineOffset));
   if (!(fine > 0.0)) fine = 1.0;
+  int top = 0;
+  while (top < levels - 1 && fine * (double)(1 << (kSubBits + top)) < rmax * (1.0 + 1e-9)) ++top;
   prm[0] = lo[0];
   prm[1] = lo[1];
   prm[2] = lo[2];
   prm[3] = fine;
+  prm[4] = (double)top;
+}
+
+// the level whose cells cover a ball of radius r (its 27 neighbours)
+__device__ __forceinline__ int cell_level(double r, const double* prm) {
+  const int top = (int)prm[4];
+  int lv = 0;
+  while (lv < top && prm[3] * (double)(1 << (kSubBits + lv)) < r * (1.0 + 1e-9)) ++lv;
+  return lv;
+}
+__device__ __forceinline__ unsigned long long level_tag(int lv) {
+  return (unsigned long long)lv << 60;
 }
 
 __device__ __forceinline__ void fine_coords(const double* p, const double* prm,
@@ -188,8 +229,8 @@ __device__ __forceinline__ void fine_coords(const double* p, const double* prm,
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     double q = floor((p[d] - prm[d]) / prm[3]);
-    q = fmin(fmax(q, 0.0), (double)((1 << kFineBits) - 32));
-    f[d] = (unsigned long long)q + (1ull << kSubBits);  // coarse coordinate >= 1
+    q = fmin(fmax(q, 0.0), (double)((1 << kFineBits) - 2 * kFineOffset));
+    f[d] = (unsigned long long)q + kFineOffset;  // coarse coordinate >= 1 at every level
   }
 }
 
@@ -227,16 +268,21 @@ __device__ __forceinline__ int64_t hash_slot(unsigned long long* hkey, int64_t c
 }
 
 __global__ void hash_insert(const unsigned long long* __restrict__ skey, int64_t n,
-                            unsigned long long* hkey, int32_t* hst, int32_t* hen, int64_t cap) {
+                            const double* __restrict__ prm, unsigned long long* hkey, int32_t* hst,
+                            int32_t* hen, int64_t cap) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const unsigned long long ck = skey[i] >> (3 * kSubBits);
-  const bool head = i == 0 || (skey[i - 1] >> (3 * kSubBits)) != ck;
-  const bool tail = i == n - 1 || (skey[i + 1] >> (3 * kSubBits)) != ck;
-  if (!head && !tail) return;
-  const int64_t h = hash_slot(hkey, cap, ck);
-  if (head) hst[h] = (int32_t)i;
-  if (tail) hen[h] = (int32_t)(i + 1);
+  const int top = (int)prm[4];
+  for (int lv = 0; lv <= top; ++lv) {
+    const int sh = 3 * (kSubBits + lv);
+    const unsigned long long ck = skey[i] >> sh;
+    const bool head = i == 0 || (skey[i - 1] >> sh) != ck;
+    const bool tail = i == n - 1 || (skey[i + 1] >> sh) != ck;
+    if (!head && !tail) continue;
+    const int64_t h = hash_slot(hkey, cap, ck | level_tag(lv));
+    if (head) hst[h] = (int32_t)i;
+    if (tail) hen[h] = (int32_t)(i + 1);
+  }
 }
 
 __device__ __forceinline__ bool hash_find(const unsigned long long* __restrict__ hkey,
@@ -290,11 +336,13 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
   constexpr bool FILL = MODE == 1;
   __shared__ double4 tile[4][kTile];
   __shared__ int32_t tid_[4][kTile];
+  __shared__ int32_t cell_st[4][64], cell_en[4][64];   // compacted union cells per warp
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = g < n_ctr;
   double cx = 0.0, cy = 0.0, cz = 0.0, rad2 = -1.0;
   unsigned long long ccx = 0, ccy = 0, ccz = 0, ckey = kEmpty;
+  int lv = 0;                          // this center's cell level
   if (valid) {
     const int64_t ic = order[g];
     cx = ctr[3 * ic];
@@ -306,10 +354,11 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     const double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
     unsigned long long f[3];
     fine_coords(pl, prm_l, f);
-    ccx = f[0] >> kSubBits;
-    ccy = f[1] >> kSubBits;
-    ccz = f[2] >> kSubBits;
-    ckey = morton3(ccx, ccy, ccz);
+    lv = cell_level(r, prm);
+    ccx = f[0] >> (kSubBits + lv);
+    ccy = f[1] >> (kSubBits + lv);
+    ccz = f[2] >> (kSubBits + lv);
+    ckey = morton3(ccx, ccy, ccz) | level_tag(lv);
   }
   int32_t* row = (FILL && valid && nidx) ? nidx + nptr[g] : nullptr;
   // SELL-32x4 column of this row as int4 blocks: block b at sblk[32 b]
@@ -390,10 +439,10 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
       if (nb >= ncell) break;
     }
   };
-  auto lookup = [&](unsigned long long x, unsigned long long y, unsigned long long z, int& st,
-                    int& en) {
+  auto lookup = [&](unsigned long long x, unsigned long long y, unsigned long long z, int level,
+                    int& st, int& en) {
     st = en = 0;
-    if (!hash_find(hkey, hst, hen, cap, morton3(x, y, z), st, en)) en = st;
+    if (!hash_find(hkey, hst, hen, cap, morton3(x, y, z) | level_tag(level), st, en)) en = st;
   };
   // Union mode: when the warp's centers sit in a small block of cells, every
   // lane scans the union of their neighbourhoods at once (all lanes busy);
@@ -409,29 +458,56 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     }
   }
   const unsigned long long ex = hi[0] - lo[0] + 3, ey = hi[1] - lo[1] + 3, ez = hi[2] - lo[2] + 3;
-  if (ex * ey * ez <= 64) {
+  // union mode needs one cell level for the whole warp
+  int lv_lo = valid ? lv : kLevels, lv_hi = valid ? lv : -1;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    lv_lo = min(lv_lo, __shfl_xor_sync(0xffffffffu, lv_lo, off));
+    lv_hi = max(lv_hi, __shfl_xor_sync(0xffffffffu, lv_hi, off));
+  }
+  // Union of up to 128 cells, of which at most 64 non-empty: their ranges are
+  // compacted (cell order kept) into lane c % 32, slot c / 32
+  bool use_union = false;
+  int stA = 0, enA = 0, stB = 0, enB = 0, n_ne = 0;
+  if (lv_lo >= lv_hi && ex * ey * ez <= 128) {
     const int ncell = (int)(ex * ey * ez);
-    int stA = 0, enA = 0, stB = 0, enB = 0;
-    for (int slot = 0; slot < 2; ++slot) {
+    for (int slot = 0; slot < 4; ++slot) {
       const int c = lane + 32 * slot;
+      int st = 0, en = 0;
       if (c < ncell) {
         const unsigned long long ix = c / (ey * ez), iy = (c / ez) % ey, iz = c % ez;
-        int st, en;
-        lookup(lo[0] - 1 + ix, lo[1] - 1 + iy, lo[2] - 1 + iz, st, en);
-        if (slot == 0) { stA = st; enA = en; } else { stB = st; enB = en; }
+        lookup(lo[0] - 1 + ix, lo[1] - 1 + iy, lo[2] - 1 + iz, lv_hi < 0 ? 0 : lv_hi, st, en);
       }
+      const unsigned ne = __ballot_sync(0xffffffffu, en > st);
+      const int at = n_ne + __popc(ne & ((1u << lane) - 1u));
+      if (en > st && at < 64) {
+        cell_st[wib][at] = st;
+        cell_en[wib][at] = en;
+      }
+      n_ne += __popc(ne);
     }
+    __syncwarp();
+    use_union = n_ne <= 64;
+    if (use_union) {
+      if (lane < n_ne) { stA = cell_st[wib][lane]; enA = cell_en[wib][lane]; }
+      if (lane + 32 < n_ne) { stB = cell_st[wib][lane + 32]; enB = cell_en[wib][lane + 32]; }
+    }
+    __syncwarp();
+  }
+  if (use_union) {
     if (MODE == 2) {
       int64_t tot = (int64_t)(enA - stA) + (enB - stB);
       for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
       ub = tot;
-    } else {
-      run_cells(ncell, stA, enA, stB, enB, valid);
+    } else if (n_ne > 0) {
+      run_cells(n_ne, stA, enA, stB, enB, valid);
     }
   } else {
     // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
-    const unsigned long long prev = __shfl_up_sync(0xffffffffu, ckey, 1);
-    unsigned heads = __ballot_sync(0xffffffffu, valid && (lane == 0 || prev != ckey));
+    // one head per distinct (cell, level): lanes of one cell need not be
+    // adjacent when their levels differ
+    const unsigned peers = __match_any_sync(0xffffffffu, ckey);
+    unsigned heads = __ballot_sync(0xffffffffu, valid && lane == __ffs(peers) - 1);
     while (heads) {
       const int a = __ffs(heads) - 1;
       heads &= heads - 1;
@@ -439,8 +515,10 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
       const unsigned long long bx = __shfl_sync(0xffffffffu, ccx, a);
       const unsigned long long by = __shfl_sync(0xffffffffu, ccy, a);
       const unsigned long long bz = __shfl_sync(0xffffffffu, ccz, a);
+      const int bl = __shfl_sync(0xffffffffu, lv, a);
       int st = 0, en = 0;
-      if (lane < 27) lookup(bx + (lane / 9) - 1, by + ((lane / 3) % 3) - 1, bz + (lane % 3) - 1, st, en);
+      if (lane < 27)
+        lookup(bx + (lane / 9) - 1, by + ((lane / 3) % 3) - 1, bz + (lane % 3) - 1, bl, st, en);
       if (MODE == 2) {
         int64_t tot = en - st;
         for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
@@ -606,7 +684,7 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     int nb = (int)std::min<int64_t>((n_src + n_ctr + 255) / 256, 148 * 8);
     bounds_kernel<<<nb, 256, 0, st>>>(src_xyz, n_src, ctr_xyz, radius, n_ctr, mm);
   }
-  grid_params<<<1, 1, 0, st>>>(mm, prm);
+  grid_params<<<1, 1, 0, st>>>(mm, prm, n_src <= kMultiLevelMaxSources ? kLevels : 1);
   size_t tb = L.tmp_bytes;
   if (n_src > 0) {
     key_kernel<<<(int)((n_src + 255) / 256), 256, 0, st>>>(src_xyz, n_src, prm, skey_in, sval_in);
@@ -616,7 +694,7 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
   }
   hash_clear<<<(int)((L.cap + 255) / 256), 256, 0, st>>>(hkey, L.cap);
   if (n_src > 0)
-    hash_insert<<<(int)((n_src + 255) / 256), 256, 0, st>>>(skey, n_src, hkey, hst, hen, L.cap);
+    hash_insert<<<(int)((n_src + 255) / 256), 256, 0, st>>>(skey, n_src, prm, hkey, hst, hen, L.cap);
   if (n_ctr > 0) {
     key_kernel<<<(int)((n_ctr + 255) / 256), 256, 0, st>>>(ctr_xyz, n_ctr, prm, ckey_in, cval_in);
     tb = L.tmp_bytes;
