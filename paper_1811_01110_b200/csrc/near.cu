@@ -370,31 +370,48 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
   // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
   // c % 32, slot c / 32) through the tile; lanes with `mine` test them all.
   auto run_cells = [&](int ncell, int stA, int enA, int stB, int enB, bool mine) {
-    auto range = [&](int c, int& cs, int& ce) {
-      const int s0 = __shfl_sync(0xffffffffu, stA, c & 31), e0 = __shfl_sync(0xffffffffu, enA, c & 31);
-      const int s1 = __shfl_sync(0xffffffffu, stB, c & 31), e1 = __shfl_sync(0xffffffffu, enB, c & 31);
-      cs = c < 32 ? s0 : s1;
-      ce = c < 32 ? e0 : e1;
-    };
-    int fill = 0, nb = 0, pos = 0, cs, ce;
-    range(0, cs, ce);
-    while (true) {
-      while (nb < ncell && fill < kTile) {        // stage until the tile is full
-        const int take = min(ce - (cs + pos), kTile - fill);
-        for (int q = lane; q < take; q += 32) {
-          const int j = cs + pos + q;
-          tile[wib][fill + q] = sxyz[j];
-          tid_[wib][fill + q] = j;
-        }
-        fill += take;
-        pos += take;
-        if (cs + pos >= ce) {
-          ++nb;
-          pos = 0;
-          if (nb < ncell) range(nb, cs, ce);
+    // exclusive prefix of the cell sizes (cell c in lane c % 32, slot c / 32)
+    // so that a tile of candidates spanning many small cells is staged with
+    // all its loads in flight at once (one latency per tile, not per cell)
+    const int szA = lane < ncell ? enA - stA : 0;
+    const int szB = lane + 32 < ncell ? enB - stB : 0;
+    int incA = szA, incB = szB;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, incA, off);
+      const int b = __shfl_up_sync(0xffffffffu, incB, off);
+      if (lane >= off) {
+        incA += a;
+        incB += b;
+      }
+    }
+    const int totA = __shfl_sync(0xffffffffu, incA, 31);
+    const int total = totA + __shfl_sync(0xffffffffu, incB, 31);
+    __syncwarp();
+    cell_en[wib][lane] = incA - szA;             // cell_en now holds the prefix
+    cell_en[wib][lane + 32] = totA + incB - szB;
+    cell_st[wib][lane] = stA;
+    cell_st[wib][lane + 32] = stB;
+    __syncwarp();
+    const int nc = min(ncell, 64);
+    for (int base = 0; base < total; base += kTile) {
+      const int fill = min(kTile, total - base);
+#pragma unroll
+      for (int r = 0; r < kTile / 32; ++r) {
+        const int q = lane + 32 * r;
+        if (q < fill) {
+          const int t = base + q;
+          int lo_c = 0, hi_c = nc - 1;               // last cell with prefix <= t
+          while (lo_c < hi_c) {
+            const int mid = (lo_c + hi_c + 1) >> 1;
+            if (cell_en[wib][mid] <= t) lo_c = mid;
+            else hi_c = mid - 1;
+          }
+          const int j = cell_st[wib][lo_c] + (t - cell_en[wib][lo_c]);
+          tile[wib][q] = sxyz[j];
+          tid_[wib][q] = j;
         }
       }
-      if (fill == 0) break;
       __syncwarp();
       if (mine) {
         // test 32 staged candidates into a per-lane bit mask, then append only
@@ -435,8 +452,6 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
         }
       }
       __syncwarp();
-      fill = 0;
-      if (nb >= ncell) break;
     }
   };
   auto lookup = [&](unsigned long long x, unsigned long long y, unsigned long long z, int level,
