@@ -233,6 +233,30 @@ def test_near_lists_edge_cases():
     assert sorted(u2i.tolist()) == o2i.tolist()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("spread", [2.0, 7.0, 40.0])
+def test_near_lists_mixed_radii_levels(spread):
+    """Radii spanning `spread`x: centers search cells of different levels (up to
+    four, the fine grid following the smallest radius; beyond 8x the smallest
+    radii share level 0), warps mix levels (per-cell mode, one head per distinct
+    (cell, level)), and clustered points make union tiles span many small cells.
+    Membership must equal the oracle's exactly."""
+    rng = np.random.default_rng(int(spread * 10))
+    n = 40000
+    # a dense cluster and a sparse background, radii from 0.004 to 0.004 * spread
+    src = np.vstack([rng.normal(scale=0.05, size=(n // 2, 3)), rng.uniform(-1, 1, (n // 2, 3))])
+    ctr = src[rng.permutation(n)[: n // 2]] + rng.normal(scale=1e-3, size=(n // 2, 3))
+    rad = 0.004 * np.exp(rng.uniform(0.0, np.log(spread), size=n // 2))
+    near = build_near_lists(ctr, src, rad)
+    uptr, uidx = near.to_user_csr()
+    optr, oidx = oracle.near_csr(ctr, rad, src)
+    assert np.array_equal(uptr, optr)
+    assert all(np.array_equal(a, b) for a, b in zip(sorted_rows(uptr, uidx),
+                                                    sorted_rows(optr, oidx)))
+    # the bound-sized SELL holds every row: CSR derived from it equals the rows
+    assert near.n_pairs == len(oidx)
+
+
 # --- config-level parity ------------------------------------------------------------
 def _case_parity(case, tol, subset=None, generic=False):
     near = build_near_lists(case.centers, case.sources, case.near_radii)
