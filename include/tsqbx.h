@@ -173,7 +173,9 @@ int tsqbx_validate(const double* packed, int64_t n_src,
  *   tsqbx_near_fill : writes every row straight into its slice (slots past a
  *       row's length are never read), then near_ptr and totals[0] = n_pairs.
  *       The CSR entries, when needed, come from tsqbx_sell_to_csr.
- * totals is a device int64[2].
+ * totals is a device int64[2].  tsqbx_near_count synchronises `stream` once,
+ * after the bounding box, to radix-sort only the Morton key bits in use; the
+ * rest of both phases is stream-ordered.
  * ------------------------------------------------------------------------- */
 int64_t tsqbx_near_workspace_bytes(int64_t n_ctr, int64_t n_src);
 int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,

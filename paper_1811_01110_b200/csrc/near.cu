@@ -18,6 +18,9 @@
 //      own members to its SELL column (4-byte stores); CSR entries on demand
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cmath>
+
 #include "common.cuh"
 
 namespace tsqbx {
@@ -700,11 +703,36 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     bounds_kernel<<<nb, 256, 0, st>>>(src_xyz, n_src, ctr_xyz, radius, n_ctr, mm);
   }
   grid_params<<<1, 1, 0, st>>>(mm, prm, n_src <= kMultiLevelMaxSources ? kLevels : 1);
+  // Radix-sort only the key bits in use: one read-back of the grid (the
+  // caller synchronises after this call anyway) halves the sort passes of a
+  // compact geometry (C2: 9 bits per axis, 27-bit keys, 4 passes instead of 8)
+  int key_bits = 3 * kFineBits;
+  if (n_src + n_ctr > 0) {
+    long long hm[8];
+    double hp[8];
+    cudaError_t e0 = cudaMemcpyAsync(hm, mm, 8 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    if (e0 == cudaSuccess)
+      e0 = cudaMemcpyAsync(hp, prm, 5 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize(st);
+    if (e0 != cudaSuccess) return check_cuda(e0, "near_count grid read-back");
+    int bits = 1;
+    for (int d = 0; d < 3; ++d) {
+      const double lo = hp[d], hi = hm[3 + d] >= 0 ? __builtin_bit_cast(double, hm[3 + d])
+                                                   : __builtin_bit_cast(double, hm[3 + d] ^ 0x7fffffffffffffffLL);
+      double q = std::floor((hi - lo) / hp[3]);
+      q = std::min(std::max(q, 0.0), (double)((1 << kFineBits) - 2 * kFineOffset));
+      const unsigned long long fmax = (unsigned long long)q + kFineOffset + 1;
+      int b = 1;
+      while (b < kFineBits && (fmax >> b) != 0) ++b;
+      bits = std::max(bits, b);
+    }
+    key_bits = 3 * bits;
+  }
   size_t tb = L.tmp_bytes;
   if (n_src > 0) {
     key_kernel<<<(int)((n_src + 255) / 256), 256, 0, st>>>(src_xyz, n_src, prm, skey_in, sval_in);
     cub::DeviceRadixSort::SortPairs(tmp, tb, skey_in, skey, sval_in, src_perm, (int)n_src, 0,
-                                    3 * kFineBits, st);
+                                    key_bits, st);
     gather_sorted<<<(int)((n_src + 255) / 256), 256, 0, st>>>(src_xyz, src_perm, n_src, sxyz);
   }
   hash_clear<<<(int)((L.cap + 255) / 256), 256, 0, st>>>(hkey, L.cap);
@@ -714,7 +742,7 @@ int tsqbx_near_count(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     key_kernel<<<(int)((n_ctr + 255) / 256), 256, 0, st>>>(ctr_xyz, n_ctr, prm, ckey_in, cval_in);
     tb = L.tmp_bytes;
     cub::DeviceRadixSort::SortPairs(tmp, tb, ckey_in, ckey, cval_in, ctr_order, (int)n_ctr, 0,
-                                    3 * kFineBits, st);
+                                    key_bits, st);
     if (!sell_ptr)
       sweep_cell_kernel<0><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
           ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey, hst, hen, L.cap, cnt, nullptr,
