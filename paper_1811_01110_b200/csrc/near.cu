@@ -5,17 +5,20 @@
 // tree lists, driver.py:197-228 / ilists.py:93-218; the closest analogue is
 // cKDTree.query_ball_point, costmodel.py:361-365).
 //
-// Pipeline (all stream-ordered; the caller reads the two totals once):
-//   1. bounding box + max radius           (block-reduced ordered-int atomics)
-//   2. fine Morton keys of sources/centers  (21 bits/axis; coarse cell = fine >> 3)
-//   3. CUB radix sort of both               -> src_perm, ctr_order ("tree leaf" order)
-//   4. open-addressed hash: coarse cell -> [start, end) in the sorted sources
-//   5. count: one warp per 32 consecutive centers sweeps the union of their
-//      neighbour cells (or each distinct cell's 27 neighbours) through a
-//      shared-memory tile; per-lane member counts
+// Pipeline (stream-ordered but for one read-back of the bounding box; the
+// caller reads the totals once):
+//   1. bounding box, min/max radius        (block-reduced ordered-int atomics)
+//   2. fine Morton keys of sources/centers  (<= 21 bits/axis; a level-L cell is
+//      the key prefix fine >> (3 + L), L chosen per center from its radius)
+//   3. CUB radix sort of both over the key bits in use
+//                                           -> src_perm, ctr_order ("tree leaf" order)
+//   4. open-addressed hash: (cell, level) -> [start, end) in the sorted sources
+//   5. bound (SELL) or count (CSR): one warp per 32 consecutive centers sweeps
+//      the union of their neighbour cells (or each distinct cell's 27
+//      neighbours) through a shared-memory tile
 //   6. CUB exclusive scans -> near_ptr, SELL-32x4 slice offsets, totals
 //   7. fill: the same sweep; per-lane member bit masks, each lane appends its
-//      own members to its SELL column (4-byte stores); CSR entries on demand
+//      own members to its SELL column (16-byte blocks); CSR entries on demand
 #include <cub/cub.cuh>
 
 #include <algorithm>
