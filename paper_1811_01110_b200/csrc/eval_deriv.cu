@@ -20,19 +20,39 @@ namespace tsqbx {
 //   r = 0 conventions as the reference: cos g := 1, t^ := s^ (_core.pyx:241-242,
 //   262-264, 285-288, 400-408).
 // ---------------------------------------------------------------------------
+// Laplace S'/D run the kappa-scaled recurrence of common.cuh (X_n = G_n / kappa_n,
+// U_n = T_n / kappa_n: U_{n+1} = alpha_n A U_n - B U_{n-1}, 3 DP per order) and
+// carry the P' ladder divided by rho (W_n = E_n / rho, Y_n = (F_n - delta_n) / rho:
+// W_{n+1} = B W_{n-1} + (2n+1) kappa_n U_n, 2 DP per order); the sums use the
+// constant weights kd = (n+1) kappa_n, kn = n kappa_n, ke = (2n+1) kappa_n.
+#ifndef TSQBX_LAP_DERIV_MINB
+#define TSQBX_LAP_DERIV_MINB 2   // CTAs per SM requested from ptxas (Laplace S'/D)
+#endif
+
 struct Bonnet {
   double a[TSQBX_MAX_ORDER + 2], b[TSQBX_MAX_ORDER + 2];
-  constexpr Bonnet() : a(), b() {
+  double kap[TSQBX_MAX_ORDER + 2], alp[TSQBX_MAX_ORDER + 2];
+  double kd[TSQBX_MAX_ORDER + 2], kn[TSQBX_MAX_ORDER + 2], ke[TSQBX_MAX_ORDER + 2];
+  constexpr Bonnet() : a(), b(), kap(), alp(), kd(), kn(), ke() {
     for (int n = 0; n < TSQBX_MAX_ORDER + 2; ++n) {
       a[n] = double(2 * n + 1) / double(n + 1);
       b[n] = double(n) / double(n + 1);
+    }
+    kap[0] = 1.0;
+    kap[1] = 1.0;
+    for (int n = 1; n + 1 < TSQBX_MAX_ORDER + 2; ++n) kap[n + 1] = b[n] * kap[n - 1];
+    for (int n = 1; n + 1 < TSQBX_MAX_ORDER + 2; ++n) alp[n] = a[n] * kap[n] / kap[n + 1];
+    for (int n = 0; n < TSQBX_MAX_ORDER + 2; ++n) {
+      kd[n] = double(n + 1) * kap[n];
+      kn[n] = double(n) * kap[n];
+      ke[n] = double(2 * n + 1) * kap[n];
     }
   }
 };
 static __constant__ Bonnet c_bon = Bonnet();
 
 template <int P, int NT, int VARIANT>
-__global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_DERIV_MINB) laplace_deriv_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[kSlots * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.n_ctr) return;
@@ -91,47 +111,54 @@ __global__ void __launch_bounds__(kSellBlock, 512 / kSellBlock) laplace_deriv_se
           const double nth = r0 ? nts : ntt[q];
           double S1 = 0.0, S2 = 0.0;
           if constexpr (P >= 1) {
-            double Gm = cg, Fm = 1.0;                          // G_1, F_1
-            S1 = Gm;
-            S2 = Fm;
+            // S1 = sum n G_n = sum kn_n X_n;  S2 = sum F_n = rho sum Y_n + sum_{odd n} B^((n-1)/2)
+            double Xm = cg, Ym = 0.0;                          // X_1 = G_1, Y_1
+            S1 = Xm;
+            double Sy = 0.0;
             if constexpr (P >= 2) {
-              double Gc = 0.5 * fma(3.0 * cg, A, -rho), Fc = 3.0 * A;   // G_2, F_2
-              S1 = fma(2.0, Gc, S1);
-              S2 += Fc;
+              double Xc = fma(3.0 * cg, A, -rho), Yc = 3.0 * cg;   // X_2 = G_2 / kappa_2, Y_2
+              S1 = fma(c_bon.kn[2], Xc, S1);
+              Sy = Yc;
 #pragma unroll
               for (int n = 2; n < P; ++n) {
-                const double Gn = fma(c_bon.a[n] * A, Gc, -(c_bon.b[n] * B) * Gm);
-                const double Fn = fma(B, Fm, (2.0 * n + 1.0) * rho * Gc);
-                Gm = Gc;
-                Gc = Gn;
-                Fm = Fc;
-                Fc = Fn;
-                S1 = fma(double(n + 1), Gn, S1);
-                S2 += Fn;
+                const double Xn = fma(c_bon.alp[n] * A, Xc, -(B * Xm));
+                const double Yn = fma(B, Ym, c_bon.ke[n] * Xc);
+                Xm = Xc;
+                Xc = Xn;
+                Ym = Yc;
+                Yc = Yn;
+                S1 = fma(c_bon.kn[n + 1], Xn, S1);
+                Sy += Yn;
               }
             }
+            double gs = 1.0;                                   // F_1's ladder: 1 + B + B^2 ...
+#pragma unroll
+            for (int i = 1; i <= (P - 1) / 2; ++i) gs = fma(gs, B, 1.0);
+            S2 = fma(rho, Sy, gs);
           }
           sval = fma(nth, S1, (nts - nth * cg) * S2);
         } else {
           const double nst = r0 ? nss
                                 : fma(n4.z, tz[q], fma(n4.y, ty[q], n4.x * tx[q])) * ir[q];
-          double Tm = 1.0, Em = 0.0;                           // T_0, E_0
+          // S1 = sum (n+1) T_n = sum kd_n U_n;  S2 = sum E_n = rho sum W_n
+          double Um = 1.0, Wm = 0.0;                           // U_0, W_0
           double S1 = 1.0, S2 = 0.0;
           if constexpr (P >= 1) {
-            double Tc = A, Ec = rho;                           // T_1, E_1
-            S1 = fma(2.0, Tc, S1);
-            S2 += Ec;
+            double Uc = A, Wc = 1.0;                           // U_1, W_1 = E_1 / rho
+            S1 = fma(2.0, Uc, S1);
+            double Sw = Wc;
 #pragma unroll
             for (int n = 1; n < P; ++n) {
-              const double Tn = fma(c_bon.a[n] * A, Tc, -(c_bon.b[n] * B) * Tm);
-              const double En = fma(B, Em, (2.0 * n + 1.0) * rho * Tc);
-              Tm = Tc;
-              Tc = Tn;
-              Em = Ec;
-              Ec = En;
-              S1 = fma(double(n + 2), Tn, S1);
-              S2 += En;
+              const double Un = fma(c_bon.alp[n] * A, Uc, -(B * Um));
+              const double Wn = fma(B, Wm, c_bon.ke[n] * Uc);
+              Um = Uc;
+              Uc = Un;
+              Wm = Wc;
+              Wc = Wn;
+              S1 = fma(c_bon.kd[n + 1], Un, S1);
+              Sw += Wn;
             }
+            S2 = rho * Sw;
           }
           sval = fma(-nss, S1, (nst - nss * cg) * S2);
         }
