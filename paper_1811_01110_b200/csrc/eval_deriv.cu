@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
         if (VARIANT == 1) {
           double jp = n == 0 ? -jn[1] : jn[n - 1] - (n + 1.0) * invx * jn[n];
           if (!(rr > 0.0)) jp = (n == 1 && ok) ? 1.0 / 3.0 : 0.0;
-          CFA(n, q) = tw * k * jp;                        // multiplies nt.t^ P_n h_n
+          CFA(n, q) = tw * k * jp * c_bon.kap[n];         // multiplies nt.t^ U_n h_n
           CFB(n, q) = rr > 0.0 ? tw * jn[n] * ir : 0.0;   // multiplies (...) P'_n h_n
         } else {
           CFA(n, q) = tw * jn[n];               // (D allocates only the first term)
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
       }
 #pragma unroll
       for (int n = 1; n <= P; ++n) {
-        // here (hm, hc) = (h_{n-1}, h_n); P_n = pc, P'_n = dc
+        // here (hm, hc) = (h_{n-1}, h_n); P_n = pc (S': kappa_n pc), P'_n = dc
         double hpr = 0.0, hpi = 0.0;
         if (VARIANT == 2) {
           const double f = (n + 1.0) * invx;
@@ -299,8 +299,16 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
             bi_[q] = fma(cb, hci, bi_[q]);
           }
           if (n < P) {
-            const double pn = fma(c_bon.a[n] * cg[q], pc[q], -c_bon.b[n] * pm[q]);
-            const double dn = fma(2.0 * n + 1.0, pc[q], dm[q]);
+            // S': kappa-scaled Legendre (pc = U_n = P_n / kappa_n, kappa_n folded
+            // into CFA); D weights P_n and P'_n with the same CFA, so it keeps P_n
+            double pn, dn;
+            if (VARIANT == 1) {
+              pn = fma(c_bon.alp[n] * cg[q], pc[q], -pm[q]);
+              dn = fma(c_bon.ke[n], pc[q], dm[q]);        // P'_{n+1} = P'_{n-1} + (2n+1) P_n
+            } else {
+              pn = fma(c_bon.a[n] * cg[q], pc[q], -c_bon.b[n] * pm[q]);
+              dn = fma(2.0 * n + 1.0, pc[q], dm[q]);
+            }
             pm[q] = pc[q];
             pc[q] = pn;
             dm[q] = dc[q];
