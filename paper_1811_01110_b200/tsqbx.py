@@ -342,8 +342,12 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
         prep.launch(torch.view_as_real(res), validate)
-    if not sync:
-        return PendingPotentials(prep, res, out, host_out, validate)
+    pinned_out = isinstance(out, torch.Tensor) and out.device.type == "cpu" and out.is_pinned()
+    if not sync or (prep.n_tgt and (pinned_out or (out is None and host_out))):
+        # the potentials and the error key come back in one stream-ordered pass
+        # (one synchronisation instead of one for the key and one for the copy)
+        pend = PendingPotentials(prep, res, out, host_out, validate)
+        return pend if not sync else pend.result()
     if prep.n_tgt and validate:
         prep.check_errors(batch_context=True)
     return _deliver(res, out, host_out)
