@@ -257,6 +257,24 @@ def test_near_lists_mixed_radii_levels(spread):
     assert near.n_pairs == len(oidx)
 
 
+@pytest.mark.gpu
+def test_near_lists_wide_extent_full_key_bits():
+    """Clusters 1e6 apart with small radii: the fine grid is capped by the
+    extent (2^21 cells per axis), the sort uses all 63 key bits, and cells far
+    larger than the radii still give the oracle's membership."""
+    rng = np.random.default_rng(5)
+    offs = np.array([[0.0, 0.0, 0.0], [1e6, -3e5, 2e5], [-7e5, 9e5, -1e6]])
+    src = np.vstack([o + rng.normal(scale=0.02, size=(3000, 3)) for o in offs])
+    ctr = src[::2] + rng.normal(scale=1e-3, size=src[::2].shape)
+    rad = rng.uniform(0.005, 0.03, size=len(ctr))
+    near = build_near_lists(ctr, src, rad)
+    uptr, uidx = near.to_user_csr()
+    optr, oidx = oracle.near_csr(ctr, rad, src)
+    assert np.array_equal(uptr, optr)
+    assert all(np.array_equal(a, b) for a, b in zip(sorted_rows(uptr, uidx),
+                                                    sorted_rows(optr, oidx)))
+
+
 # --- config-level parity ------------------------------------------------------------
 def _case_parity(case, tol, subset=None, generic=False):
     near = build_near_lists(case.centers, case.sources, case.near_radii)
