@@ -138,6 +138,12 @@ constexpr int kSellBlock = TSQBX_SELL_BLOCK;   // threads per CTA of the SELL ke
 #ifndef TSQBX_LAP_MINB
 #define TSQBX_LAP_MINB 3
 #endif
+// two targets per center with uniform target runs (no tgt_ptr registers): one
+// more CTA per SM despite a few spilled loop invariants (C2 dense +2.9 %,
+// C2 literal +6 %; the general-tgt_ptr kernel spills twice as much and keeps 3)
+#ifndef TSQBX_LAP_MINB_UNI
+#define TSQBX_LAP_MINB_UNI 4
+#endif
 // one target per center (C1, C4, C5): one more CTA per SM (measured: C4
 // literal +9 %, C5 literal +12 %, dense -1 %; with two targets it costs 2-40 %)
 #ifndef TSQBX_LAP_MINB1

@@ -195,7 +195,7 @@ namespace tsqbx {
 #endif
 
 template <int P, int NT, bool VAL, int S, int UNI>
-__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB) laplace_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : (UNI > 0 ? TSQBX_LAP_MINB_UNI : TSQBX_LAP_MINB)) laplace_sell_kernel(const EvalParams a) {
   CTA_START();
   __shared__ int4 ring[kSlots * kSellBlock];
   constexpr int kRowsPerWarp = 32 / S;
