@@ -59,18 +59,23 @@ def pick_group_lanes(mean_len: float) -> int:
     return max(1, min(32, g))
 
 
-def pick_split(mean_len: float, n_rows: int, one_target: bool, sms: int = 148) -> int:
+def pick_split(mean_len: float, n_rows: int, one_target: bool, sms: int = 148,
+               uniform: bool = False) -> int:
     """Threads per row on the SELL layout (Laplace S): long rows are split over
     2 threads of a warp (shorter work units: C2 dense +3.5 %, C4 dense +4 %),
-    over 4 when the rows do not fill one wave of the GPU (C1 dense 2.7x); short
-    rows (literal presets) are not split.  GIGAQBX_SPLIT overrides."""
+    over 4 when the rows fill less than ~1.5 waves of the GPU (C1 dense 2.7x); short
+    rows (literal presets) are not split.  A wave is 4 CTAs of 256 threads per
+    SM for one target per center or uniform target runs, else 3.
+    GIGAQBX_SPLIT overrides."""
     env = os.environ.get("GIGAQBX_SPLIT")
     if env:
         return int(env)
     if mean_len < 48:
         return 1
-    waves = n_rows / (sms * (1024 if one_target else 768))
-    return 4 if waves < 1.0 else 2
+    waves = n_rows / (sms * (1024 if (one_target or uniform) else 768))
+    # 4 threads per row until ~1.5 waves (C2 geometry, 4-CTA kernel: 196 k rows =
+    # 1.3 waves 0.213 vs 0.223 ms; 262 k rows = 1.7 waves equal)
+    return 4 if waves < 1.5 else 2
 
 
 def pick_layout() -> str:
@@ -154,6 +159,8 @@ class _Prepared:
         self.real_w = False
         self.one_target = os.environ.get("GIGAQBX_ONE_TARGET", "0") == "1"
         self.tuni = 0         # k > 0: every row owns k consecutive targets (set_uniform_targets)
+        self._auto_split = (not group_lanes and self.layout == "sell" and spec.is_laplace
+                            and self.variant == 0 and "GIGAQBX_SPLIT" not in os.environ)
 
     def set_uniform_targets(self, known: bool = False) -> None:
         """Let the SELL kernels address row g's targets as [k g, k g + k) instead of
@@ -165,6 +172,11 @@ class _Prepared:
         if known or bool(torch.equal(self.tptr, torch.arange(
                 self.n_ctr + 1, dtype=torch.int64, device=self.dev) * k)):
             self.tuni = k
+            if self._auto_split:          # the uniform kernel fits one more CTA per SM
+                self.G = pick_split(self.near.mean_len, self.n_ctr, k == 1,
+                                    dv.sm_count(self.dev.index if self.dev.index is not None
+                                                else torch.cuda.current_device()),
+                                    uniform=True)
 
     def pack(self, w: torch.Tensor) -> None:
         """(Re)pack the sources with weights ``w`` (interleaved float64 view)."""

@@ -45,5 +45,8 @@ def test_row_split_choice(monkeypatch):
     assert pick_split(12.0, 262144, False) == 1          # literal rows: never split
     assert pick_split(201.0, 262144, False) == 2         # dense, several waves
     assert pick_split(201.0, 4096, True) == 4            # dense, under one wave
+    # 200 k rows: 1.76 waves of 3 CTAs/SM, 1.32 waves of 4 (uniform target runs)
+    assert pick_split(201.0, 200000, False) == 2
+    assert pick_split(201.0, 200000, False, uniform=True) == 4
     monkeypatch.setenv("GIGAQBX_SPLIT", "1")
     assert pick_split(201.0, 262144, False) == 1
