@@ -200,8 +200,14 @@ class _Prepared:
                  | (_lib.FLAG_ONE_TARGET if self.one_target else 0))
         near = self.near
         g0, g1 = rows if rows is not None else (0, self.n_ctr)
+        G = self.G
         if self.tuni and (g0, g1) == (0, self.n_ctr):
             flags |= _lib.FLAG_UNIFORM_TARGETS | (self.tuni << 8)
+        elif self._auto_split and (g0, g1) != (0, self.n_ctr):
+            # a row range (multi-GPU shard) fills fewer waves than the whole problem
+            G = pick_split(self.near.mean_len, g1 - g0, self.n_tgt < 2 * self.n_ctr,
+                           dv.sm_count(self.dev.index if self.dev.index is not None
+                                       else torch.cuda.current_device()))
         sell = self.layout == "sell" and near.sell_ptr is not None
         if sell and g0 % 32:
             raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
@@ -215,7 +221,7 @@ class _Prepared:
             near.sell_ptr.data_ptr() + 8 * (g0 // 32) if sell else None,
             near.sell_idx.data_ptr() if sell else None, self.tgt.data_ptr(),
             dv.ptr(self.tn), self.tptr.data_ptr() + 8 * g0, self.n_tgt,
-            dv.ptr(self.tidx) if user_order else None, out_offset, flags, self.G,
+            dv.ptr(self.tidx) if user_order else None, out_offset, flags, G,
             self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.err.data_ptr(),
             dv.stream_handle(self.dev)), "tsqbx_eval_packed")
 
