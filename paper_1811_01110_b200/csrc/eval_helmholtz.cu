@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
   }
 }
 
-template <int P, int NT, bool VAL>
+// UNI = NT: uniform target runs (row g owns targets [NT g, NT g + NT)), one
+// pass and no tgt_ptr loads (TSQBX_FLAG_UNIFORM_TARGETS)
+template <int P, int NT, bool VAL, int UNI>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
   // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n, in registers
   // (a shared-memory copy measured slower)
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
   if (g < a.n_ctr) {
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const int64_t t0 = UNI > 0 ? g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];
@@ -235,7 +237,7 @@ struct HelmholtzLaunch {
   template <int NT, bool VAL>
   static void one(bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
     if (sell)
-      helmholtz_sell_kernel<P, NT, VAL>
+      (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT> : helmholtz_sell_kernel<P, NT, VAL, 0>)
           <<<(int)((n_ctr + kSellBlock - 1) / kSellBlock), kSellBlock, 0, st>>>(a);
     else
       helmholtz_s_kernel<P, NT, VAL><<<(int)((n_ctr * a.G + 255) / 256), 256, 0, st>>>(a);
