@@ -11,7 +11,7 @@ device near-list builder ``build_near_lists``.
 from ._backend import BACKEND_NAME, available_backends, get_backend
 from .kernels import Equation, KernelSpec, Variant
 from .nearlist import NearLists, build_near_lists
-from .p2p import P2PProblem, direct_sum, p2p_rows
+from .p2p import P2PProblem, direct_sum, kernel_value, p2p_rows
 from .tsqbx import (PendingPotentials, TsConfig, TsqbxProblem, ts_accumulate,
                     ts_accumulate_batch, ts_eval)
 
@@ -20,5 +20,6 @@ __version__ = "0.1.0"
 __all__ = [
     "BACKEND_NAME", "available_backends", "get_backend", "Equation", "KernelSpec", "Variant",
     "NearLists", "build_near_lists", "TsConfig", "TsqbxProblem", "ts_accumulate",
-    "ts_accumulate_batch", "ts_eval", "PendingPotentials", "P2PProblem", "direct_sum", "p2p_rows", "__version__",
+    "ts_accumulate_batch", "ts_eval", "PendingPotentials", "P2PProblem", "direct_sum",
+    "kernel_value", "p2p_rows", "__version__",
 ]

@@ -165,6 +165,39 @@ def direct_sum(spec: KernelSpec, sources, weights, targets, source_normals=None,
     return out.cpu().numpy() if _host_out(sources) else out
 
 
+_NORMAL_TOL = 1e-12     # kernels.py:23
+
+
+def _check_normal(normal, name):
+    """kernels.py:74-80: present and unit length (same ValueError texts)."""
+    if normal is None:
+        raise ValueError(f"kernel variant requires a {name} normal")
+    normal = np.asarray(normal, dtype=np.float64).reshape(3)
+    if abs(float(np.linalg.norm(normal)) - 1.0) > _NORMAL_TOL:
+        raise ValueError(f"{name} normal must be unit length")
+    return normal
+
+
+def kernel_value(spec: KernelSpec, target, source, target_normal=None,
+                 source_normal=None, device=None) -> complex:
+    """K(t, s), nu(t).grad_t K or nu(s).grad_s K at one pair (kernels.py:83-111),
+    evaluated by the GPU p2p kernel as a 1 x 1 direct sum; the reference's checks
+    and ValueError texts come first (a coincident pair is an error here, not a
+    non-finite value)."""
+    t = np.asarray(target, dtype=np.float64).reshape(3)
+    s = np.asarray(source, dtype=np.float64).reshape(3)
+    if float(np.linalg.norm(t - s)) == 0.0:
+        raise ValueError("singular point: target coincides with source")
+    tn = sn = None
+    if spec.needs_target_normals:
+        tn = _check_normal(target_normal, "target").reshape(1, 3)
+    if spec.needs_source_normals:
+        sn = _check_normal(source_normal, "source").reshape(1, 3)
+    out = direct_sum(spec, s.reshape(1, 3), np.ones(1, np.complex128), t.reshape(1, 3),
+                     source_normals=sn, target_normals=tn, device=device)
+    return complex(out[0])
+
+
 def p2p_rows(spec: KernelSpec, sources, weights, targets, row_tgt, row_ptr, row_idx,
              source_normals=None, target_normals=None, device=None):
     """Batched per-box p2p (driver.py:187-210): row r's targets see only the

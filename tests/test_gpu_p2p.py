@@ -206,3 +206,62 @@ def test_derivative_variants_match_finite_differences():
                        source_normals=nu[None])
         assert abs(sp[0] - fd_t[0]) <= 1e-8 * abs(sp[0])
         assert abs(d[0] - fd_s[0]) <= 1e-8 * abs(d[0])
+
+
+# --- kernel_value (kernels.py:83-111) ------------------------------------------------
+def _unit(v):
+    return v / np.linalg.norm(v)
+
+
+def test_kernel_value_known_answers_and_symmetry():
+    # test_kernels.py:18-48, 98-100
+    from paper_1811_01110_b200 import kernel_value
+    t, s = np.array([1.0, -0.5, 2.0]), np.array([0.1, 0.2, 0.3])
+    r = float(np.linalg.norm(t - s))
+    assert kernel_value(LAPLACE, t, s) == pytest.approx(1 / (4 * math.pi * r), rel=1e-14)
+    helm = KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=2.0)
+    assert kernel_value(helm, t, s) == pytest.approx(np.exp(2j * r) / (4 * math.pi * r),
+                                                     rel=1e-14)
+    rng = np.random.default_rng(4)
+    t, s = rng.normal(size=3), rng.normal(size=3)
+    assert kernel_value(LAPLACE, t, s) == kernel_value(LAPLACE, s, t)
+    assert kernel_value(LAPLACE, t, s).imag == 0.0
+
+
+def test_kernel_value_source_normal_deriv_on_sphere_vs_finite_differences():
+    # test_kernels.py:57-65
+    from paper_1811_01110_b200 import kernel_value
+    s_hat = _unit(np.array([0.3, 0.5, 0.81]))
+    t = 2.0 * s_hat
+    val = kernel_value(KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV), t, s_hat,
+                       source_normal=s_hat)
+    h = 1e-6
+    fd = (kernel_value(LAPLACE, t, s_hat + h * s_hat)
+          - kernel_value(LAPLACE, t, s_hat - h * s_hat)) / (2 * h)
+    assert abs(val - fd) < 1e-7 * abs(fd)
+
+
+@pytest.mark.parametrize("spec", [
+    KernelSpec(variant=Variant.TARGET_NORMAL_DERIV),
+    KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV),
+    KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=1.3, variant=Variant.TARGET_NORMAL_DERIV),
+    KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=1.3, variant=Variant.SOURCE_NORMAL_DERIV),
+])
+def test_kernel_value_derivatives_match_finite_differences(spec):
+    # test_kernels.py:68-95 (20 random pairs instead of 100)
+    from paper_1811_01110_b200 import kernel_value
+    rng = np.random.default_rng(8)
+    h = 1e-5
+    base = KernelSpec(equation=spec.equation, helmholtz_k=spec.helmholtz_k)
+    for _ in range(20):
+        t, s = rng.normal(size=3), rng.normal(size=3)
+        if np.linalg.norm(t - s) < 0.1:
+            s = t + _unit(s - t) * 0.1
+        nu = _unit(rng.normal(size=3))
+        if spec.variant is Variant.TARGET_NORMAL_DERIV:
+            val = kernel_value(spec, t, s, target_normal=nu)
+            fd = (kernel_value(base, t + h * nu, s) - kernel_value(base, t - h * nu, s)) / (2 * h)
+        else:
+            val = kernel_value(spec, t, s, source_normal=nu)
+            fd = (kernel_value(base, t, s + h * nu) - kernel_value(base, t, s - h * nu)) / (2 * h)
+        assert abs(val - fd) <= 1e-6 * max(1e-3, abs(fd))

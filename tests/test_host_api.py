@@ -50,3 +50,19 @@ def test_row_split_choice(monkeypatch):
     assert pick_split(201.0, 200000, False, uniform=True) == 4
     monkeypatch.setenv("GIGAQBX_SPLIT", "1")
     assert pick_split(201.0, 262144, False) == 1
+
+
+def test_kernel_value_checks_before_the_gpu():
+    """kernel_value (kernels.py:83-111) raises the reference's errors from the
+    host-side checks, before any device work (so these run without a GPU)."""
+    from paper_1811_01110_b200 import Equation, KernelSpec, Variant, kernel_value
+    with pytest.raises(ValueError, match="singular point: target coincides with source"):
+        kernel_value(KernelSpec(), np.ones(3), np.ones(3))
+    with pytest.raises(ValueError, match="requires a source normal"):
+        kernel_value(KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV), np.zeros(3), np.ones(3))
+    with pytest.raises(ValueError, match="requires a target normal"):
+        kernel_value(KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=1.0,
+                                variant=Variant.TARGET_NORMAL_DERIV), np.zeros(3), np.ones(3))
+    with pytest.raises(ValueError, match="source normal must be unit length"):
+        kernel_value(KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV), np.array([1.0, 0, 0]),
+                     np.zeros(3), source_normal=np.array([0.0, 0, 2.0]))
