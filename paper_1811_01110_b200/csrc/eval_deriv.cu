@@ -51,7 +51,8 @@ struct Bonnet {
 };
 static __constant__ Bonnet c_bon = Bonnet();
 
-template <int P, int NT, int VARIANT>
+// UNI = NT: uniform target runs (TSQBX_FLAG_UNIFORM_TARGETS), no tgt_ptr loads
+template <int P, int NT, int VARIANT, int UNI>
 __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_DERIV_MINB) laplace_deriv_sell_kernel(const EvalParams a) {
   __shared__ int4 ring[kSlots * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_DERIV_MINB) laplace_deri
   const bool realw = a.real_w || *a.imag_flag == 0u;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const int64_t t0 = UNI > 0 ? g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], rr[NT], ir[NT], nx[NT], ny[NT], nz[NT], ntt[NT];
     double ar[NT], ai[NT];
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_DERIV_MINB) laplace_deri
   }
 }
 
-template <int P, int NT, int VARIANT>
+template <int P, int NT, int VARIANT, int UNI>
 __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSellBlock : 1)) helmholtz_deriv_sell_kernel(const EvalParams a) {
   // per-thread target coefficients in (dynamic) shared memory, [term][n][q][thread]
   extern __shared__ double cfs[];
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSel
   const bool val = a.validate != 0;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = a.tptr[g], t1 = a.tptr[g + 1];
+  const int64_t t0 = UNI > 0 ? g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], nx[NT], ny[NT], nz[NT], ntt[NT];
@@ -364,26 +365,34 @@ void launch_deriv_p(int equation, int variant, int nt, const EvalParams& a, int6
                     cudaStream_t st) {
   const int blocks = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
   if (equation == TSQBX_EQ_LAPLACE) {
+#define LAP_DK(NT_, V_) (a.tuni == NT_ ? laplace_deriv_sell_kernel<P, NT_, V_, NT_> \
+                                          : laplace_deriv_sell_kernel<P, NT_, V_, 0>)
     if (variant == 1) {
-      if (nt >= 2) laplace_deriv_sell_kernel<P, 2, 1><<<blocks, kSellBlock, 0, st>>>(a);
-      else laplace_deriv_sell_kernel<P, 1, 1><<<blocks, kSellBlock, 0, st>>>(a);
+      if (nt >= 2) LAP_DK(2, 1)<<<blocks, kSellBlock, 0, st>>>(a);
+      else LAP_DK(1, 1)<<<blocks, kSellBlock, 0, st>>>(a);
     } else {
-      if (nt >= 2) laplace_deriv_sell_kernel<P, 2, 2><<<blocks, kSellBlock, 0, st>>>(a);
-      else laplace_deriv_sell_kernel<P, 1, 2><<<blocks, kSellBlock, 0, st>>>(a);
+      if (nt >= 2) LAP_DK(2, 2)<<<blocks, kSellBlock, 0, st>>>(a);
+      else LAP_DK(1, 2)<<<blocks, kSellBlock, 0, st>>>(a);
     }
+#undef LAP_DK
   } else {
     auto go = [&](auto kernel, int ntt, int terms) {
       const int smem = terms * (P + 1) * ntt * kSellBlock * (int)sizeof(double);
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       kernel<<<blocks, kSellBlock, smem, st>>>(a);
     };
+#define HELM_DK(NT_, V_) (a.tuni == NT_ ? helmholtz_deriv_sell_kernel<P, NT_, V_, NT_> \
+                                           : helmholtz_deriv_sell_kernel<P, NT_, V_, 0>)
     if (variant == 1) {
-      if (nt >= 2) go(helmholtz_deriv_sell_kernel<P, 2, 1>, 2, 2);
-      else go(helmholtz_deriv_sell_kernel<P, 1, 1>, 1, 2);
+      if (nt >= 2) go(HELM_DK(2, 1), 2, 2);
+      else go(HELM_DK(1, 1), 1, 2);
     } else {
-      if (nt >= 2) go(helmholtz_deriv_sell_kernel<P, 2, 2>, 2, 1);
-      else go(helmholtz_deriv_sell_kernel<P, 1, 2>, 1, 1);
+      // D keeps the tgt_ptr kernel: its uniform-target build allocates worse
+      // (C3 dense D 1.078 -> 1.159 ms)
+      if (nt >= 2) go(helmholtz_deriv_sell_kernel<P, 2, 2, 0>, 2, 1);
+      else go(helmholtz_deriv_sell_kernel<P, 1, 2, 0>, 1, 1);
     }
+#undef HELM_DK
   }
 }
 
