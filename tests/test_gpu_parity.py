@@ -651,6 +651,22 @@ def test_uniform_target_runs_flag():
     assert rp.prep.tuni == 0
     one = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.sources, near)
     assert one.prep.tuni == 1
+    # three targets per center: uniform runs, but wider than a kernel pass (NT = 2),
+    # so the kernels keep the tgt_ptr path; all equations and variants stay exact
+    rng = np.random.default_rng(2)
+    tg3 = np.repeat(case.centers, 3, axis=0) + rng.normal(scale=1e-4, size=(3 * case.n_centers, 3))
+    tp3 = np.arange(case.n_centers + 1) * 3
+    uptr, uidx = near.to_user_csr()
+    for spec, tol in ((KernelSpec(), LAP_TOL),
+                      (KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=10.0), HELM_TOL)):
+        cfg = TsConfig(spec, 8)
+        p3 = TsqbxProblem(cfg, case.sources, case.weights, case.centers, tg3, near, tgt_ptr=tp3)
+        assert p3.prep.tuni == 3
+        got = p3.evaluate(validate=True).cpu().numpy()
+        ref = oracle.ts_batch("laplace" if spec.is_laplace else "helmholtz", 0,
+                              spec.helmholtz_k or 0.0, 8, case.sources, case.weights,
+                              case.centers, uptr, uidx, tg3, tp3)
+        assert normwise(got, ref) <= tol
 
 
 @pytest.mark.gpu
