@@ -113,8 +113,17 @@ template <int P, int NT, bool VAL, int UNI>
 __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
   // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n, in registers
   // (a shared-memory copy measured slower)
-  double cfr[NT][P + 1];
-#define CF(n, q) cfr[q][n]
+  // one target per center: the coefficients live in shared memory (fewer
+  // registers, fewer spills: C5 literal +9 %, dense +2 %); with two targets the
+  // register copy is faster (C3 dense -1.5 % from shared memory)
+  constexpr bool kCfShared = NT == 1;
+  extern __shared__ double cfs[];
+  double cfr[kCfShared ? 1 : NT][kCfShared ? 1 : P + 1];
+  auto cf = [&](int n, int q) -> double& {
+    if constexpr (kCfShared) return cfs[(n * NT + q) * kSellBlock + threadIdx.x];
+    else return cfr[q][n];
+  };
+#define CF(n, q) cf(n, q)
   __shared__ int4 ring[kSlots * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g < a.n_ctr) {
@@ -237,8 +246,11 @@ struct HelmholtzLaunch {
   template <int NT, bool VAL>
   static void one(bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
     if (sell)
+    {
+      const int smem = NT == 1 ? (P + 1) * kSellBlock * (int)sizeof(double) : 0;
       (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT> : helmholtz_sell_kernel<P, NT, VAL, 0>)
-          <<<(int)((n_ctr + kSellBlock - 1) / kSellBlock), kSellBlock, 0, st>>>(a);
+          <<<(int)((n_ctr + kSellBlock - 1) / kSellBlock), kSellBlock, smem, st>>>(a);
+    }
     else
       helmholtz_s_kernel<P, NT, VAL><<<(int)((n_ctr * a.G + 255) / 256), 256, 0, st>>>(a);
   }
