@@ -179,7 +179,10 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_DERIV_MINB) laplace_deri
 }
 
 template <int P, int NT, int VARIANT, int UNI>
-__global__ void __launch_bounds__(kSellBlock, (384 / kSellBlock > 0 ? 384 / kSellBlock : 1)) helmholtz_deriv_sell_kernel(const EvalParams a) {
+// CTAs per SM requested from ptxas: D at 2 (~128 registers, some spills: C3
+// literal D +18 %, dense equal); S' at 1 (184-198 registers: 2 CTAs cost C3
+// dense S' 11 %)
+__global__ void __launch_bounds__(kSellBlock, VARIANT == 2 ? 2 : 1) helmholtz_deriv_sell_kernel(const EvalParams a) {
   // per-thread target coefficients in (dynamic) shared memory, [term][n][q][thread]
   extern __shared__ double cfs[];
   __shared__ int4 ring[kSlots * kSellBlock];
