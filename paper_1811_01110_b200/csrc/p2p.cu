@@ -156,8 +156,12 @@ __device__ __forceinline__ void p2p_stream(const P2PParams& a, SourceTile& st, i
 
 // CTA = 128 threads = (128 >> log2_tt) source lanes x (1 << log2_tt) target
 // lanes; each target lane owns TPT targets spaced by the lane count.
+// CTAs per SM requested from ptxas: 8 (64 registers) for Helmholtz and the
+// Laplace double layer (65536^2: Helmholtz S / S' / D +3 / +10 / +12 %, Laplace
+// D +8 %); the Laplace S and S' kernels keep their natural allocation (S' -23 %
+// at 8).
 template <int EQ, int VARIANT, bool PRECISE, int TPT>
-__global__ void __launch_bounds__(kP2PBlock) p2p_kernel(P2PParams a) {
+__global__ void __launch_bounds__(kP2PBlock, (EQ == TSQBX_EQ_HELMHOLTZ || VARIANT == 2) ? 8 : 1) p2p_kernel(P2PParams a) {
   __shared__ SourceTile st;
   __shared__ double2 red[kP2PBlock];
   const int tid = threadIdx.x;
