@@ -77,8 +77,9 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
   const int len = h.len;
   const int64_t t0 = h.t0, t1 = h.t1;
   // high orders have more arithmetic per source to cover a second gather in
-  // flight (measured: C4 dense p = 12 +7 %; p = 8 -2 %)
-  using Stream = SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)>;
+  // flight (measured: C4 literal p = 12 +7 %; p = 8 -2 %); split rows (S > 1,
+  // the dense presets) keep one in flight (C4 dense +2.2 %)
+  using Stream = SellStream<false, (P >= 12 && S == 1 ? 2 : TSQBX_GATHER_DEPTH)>;
   // the index ring starts filling before the target range is known
   Stream ss(a, h.soff, g, len, REALW, ring, false, part, S);
   for (int64_t tb = t0; tb < t1; tb += NT) {
