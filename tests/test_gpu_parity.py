@@ -721,3 +721,43 @@ def test_near_field_potentials_matches_oracle(pinned):
                           case.sources, case.weights, case.centers, ptr, idx, case.targets,
                           case.tgt_ptr)
     assert normwise(got, ref) <= HELM_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,variant", [("c2", Variant.SINGLE_LAYER), ("c3", Variant.SINGLE_LAYER),
+                                          ("c2", Variant.TARGET_NORMAL_DERIV),
+                                          ("c3", Variant.SOURCE_NORMAL_DERIV)])
+def test_row_range_launches_match_full(name, variant):
+    """The multi-GPU shard path: launches over row ranges (multiples of 32, each
+    with its own row split and the tgt_ptr kernels), in user order and in
+    processing order with an output offset, reproduce the whole-problem
+    evaluation (which takes the uniform-target kernels)."""
+    case = configs.make_case(name, "literal", n=8192)
+    sp = case.cfg.spec
+    cfg = TsConfig(KernelSpec(equation=sp.equation, variant=variant, helmholtz_k=sp.helmholtz_k),
+                   case.cfg.p_qbx)
+    tnrm = np.repeat(case.normals, np.diff(case.tgt_ptr), axis=0)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    prob = TsqbxProblem(cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr, source_normals=case.normals, target_normals=tnrm)
+    prep = prob.prep
+    assert prep.tuni == 2
+    full = prob.evaluate().clone()
+    tol = LAP_TOL if sp.is_laplace else HELM_TOL
+    bounds = [0, 2048, 5120, prep.n_ctr]
+    out = torch.zeros_like(full)
+    for g0, g1 in zip(bounds[:-1], bounds[1:]):
+        prep.launch(torch.view_as_real(out), False, rows=(g0, g1))
+    assert normwise(out.cpu().numpy(), full.cpu().numpy()) <= tol
+    # processing order, each range into its own buffer at offset tptr[g0]
+    tptr = prep.tptr.cpu().numpy()
+    proc = torch.zeros_like(full)
+    for g0, g1 in zip(bounds[:-1], bounds[1:]):
+        t0, t1 = int(tptr[g0]), int(tptr[g1])
+        part = torch.zeros(t1 - t0, dtype=full.dtype, device=full.device)
+        prep.launch(torch.view_as_real(part), False, rows=(g0, g1), out_offset=t0,
+                    user_order=False)
+        proc[t0:t1] = part
+    user = torch.empty_like(proc)
+    user[prep.tidx] = proc
+    assert normwise(user.cpu().numpy(), full.cpu().numpy()) <= tol
