@@ -1,6 +1,8 @@
 """Per-CTA start/end times (globaltimer) of the Laplace SELL kernel, from a
 debug build of the library with timing stores (row split):
 
+    make -C paper_1811_01110_b200/csrc OUT=$PWD/paper_1811_01110_b200/_lib/dbg_timing.so \
+        OBJDIR=/tmp/obj_dbg EXTRA_NVFLAGS=-DTSQBX_CTA_TIMING
     python tools/cta_timing_probe.py [case] [preset]     # GIGAQBX_LIB_PATH -> debug build
 """
 import ctypes
