@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 6
+#define TSQBX_ABI_VERSION 7
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -194,13 +194,17 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
  * (user center ctr_order[g] becomes row g): writes ctr_out (n_ctr x 3),
  * tptr_out (n_ctr + 1), tgt_out / tnrm_out (n_tgt x 3; tnrm only if tgt_nrm)
  * and tgt_index (processing target -> user target; pass it as tgt_out of the
- * evaluation to write potentials in user order). */
+ * evaluation to write potentials in user order).  `bad` (device int64,
+ * nullable) is set to 1 when tgt_ptr is malformed (tgt_ptr[0] != 0, a
+ * decreasing entry, an entry past n_tgt, or tgt_ptr[n_ctr] != n_tgt), else 0;
+ * malformed rows get no targets and tptr_out stays within [0, n_tgt], so a
+ * later evaluation never leaves the target arrays (the caller reports *bad). */
 int64_t tsqbx_order_workspace_bytes(int64_t n_ctr);
 int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* ctr_xyz,
                         const int64_t* tgt_ptr, const double* tgt_xyz, const double* tgt_nrm,
                         int64_t n_tgt, void* workspace, int64_t ws_bytes,
                         double* ctr_out, int64_t* tptr_out, double* tgt_out, double* tnrm_out,
-                        int64_t* tgt_index, void* stream);
+                        int64_t* tgt_index, int64_t* bad, void* stream);
 
 /* Sliced-ELL (SELL-32x4) copy of a CSR: rows in slices of 32; a slice's width
  * is its longest row rounded up to 4, and entry (row r, column i) sits at

@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import functools
+import inspect
 
 import numpy as np
 import torch
@@ -16,7 +17,41 @@ def require_cuda(device=None) -> torch.device:
                                                                        torch.cuda.current_device())
     if dev.type != "cuda":
         raise RuntimeError(f"device {dev} is not a CUDA device")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
     return dev
+
+
+def on_device(fn):
+    """Run ``fn`` with its ``device`` argument as the current CUDA device.
+
+    The C ABI launches on the current device (a stream handle does not name
+    one), so every public entry point that takes ``device=`` makes that device
+    current for the call; ``device=None`` keeps the current one."""
+    sig = inspect.signature(fn)
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        bound = sig.bind(*args, **kwargs)
+        dev = require_cuda(bound.arguments.get("device"))
+        bound.arguments["device"] = dev
+        with torch.cuda.device(dev):
+            return fn(*bound.args, **bound.kwargs)
+
+    return wrapper
+
+
+def on_own_device(fn):
+    """Method form of :func:`on_device`: the device is the object's ``dev``."""
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        if self.dev.type != "cuda":          # host-side bookkeeping only (tests)
+            return fn(self, *args, **kwargs)
+        with torch.cuda.device(self.dev):
+            return fn(self, *args, **kwargs)
+
+    return wrapper
 
 
 @functools.lru_cache(maxsize=None)

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
                                                                "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
-ABI_VERSION = 6      # TSQBX_ABI_VERSION in include/tsqbx.h
+ABI_VERSION = 7      # TSQBX_ABI_VERSION in include/tsqbx.h
 
 # status codes (include/tsqbx.h)
 OK = 0
@@ -63,7 +63,7 @@ SIGNATURES = {
     "tsqbx_validate": (_I, [_P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _P]),
     "tsqbx_order_workspace_bytes": (_I64, [_I64]),
     "tsqbx_order_targets": (_I, [_I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P,
-                                 _P]),
+                                 _P, _P]),
     "tsqbx_scatter_c128": (_I, [_I64, _P, _P, _P, _P]),
     "tsqbx_sell_to_csr": (_I, [_I64, _P, _P, _P, _P, _P]),
     "tsqbx_sell_compact": (_I, [_I64, _P, _P, _P, _P, _P]),

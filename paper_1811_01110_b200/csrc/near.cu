@@ -607,22 +607,31 @@ __global__ void sell_tail(int64_t* wid, int64_t n_sl) { wid[n_sl] = 0; }
 
 
 // --- targets into processing order -------------------------------------------
+// Per-row target counts in processing order.  Malformed caller offsets (not
+// starting at 0, decreasing, past n_tgt, or not ending at n_tgt) raise *bad and
+// give the row no targets, so nothing downstream leaves the target arrays.
 __global__ void order_count(const int32_t* __restrict__ order, const int64_t* __restrict__ tptr,
-                            int64_t n, int64_t* __restrict__ cnt) {
+                            int64_t n, int64_t n_tgt, int64_t* __restrict__ cnt,
+                            int64_t* __restrict__ bad) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g > n) return;
   if (g == n) {
     cnt[n] = 0;
+    if ((tptr[0] != 0 || tptr[n] != n_tgt) && bad) *bad = 1;
     return;
   }
   const int64_t ic = order[g];
-  cnt[g] = tptr[ic + 1] - tptr[ic];
+  const int64_t a = tptr[ic], b = tptr[ic + 1];
+  const bool ok = 0 <= a && a <= b && b <= n_tgt;
+  if (!ok && bad) *bad = 1;
+  cnt[g] = ok ? b - a : 0;
 }
 
 __global__ void order_copy(const int32_t* __restrict__ order, const double* __restrict__ ctr,
                            const int64_t* __restrict__ tptr, const double* __restrict__ tgt,
-                           const double* __restrict__ tnrm, int64_t n,
-                           const int64_t* __restrict__ tptr_out, double* __restrict__ ctr_out,
+                           const double* __restrict__ tnrm, int64_t n, int64_t n_tgt,
+                           const int64_t* __restrict__ cnt_in, int64_t* __restrict__ tptr_out,
+                           double* __restrict__ ctr_out,
                            double* __restrict__ tgt_out, double* __restrict__ tnrm_out,
                            int64_t* __restrict__ tidx) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -631,7 +640,13 @@ __global__ void order_copy(const int32_t* __restrict__ order, const double* __re
   ctr_out[3 * g] = ctr[3 * ic];
   ctr_out[3 * g + 1] = ctr[3 * ic + 1];
   ctr_out[3 * g + 2] = ctr[3 * ic + 2];
-  const int64_t src0 = tptr[ic], cnt = tptr[ic + 1] - src0, dst0 = tptr_out[g];
+  // cnt: the checked count of order_count (0 for a malformed row); with
+  // malformed offsets the prefix can pass n_tgt, so the copy and the row
+  // offsets the kernels read are clamped to the target arrays
+  const int64_t src0 = tptr[ic], dst0 = tptr_out[g];
+  const int64_t cnt = min(cnt_in[g], max((int64_t)0, n_tgt - dst0));
+  if (dst0 > n_tgt) tptr_out[g] = n_tgt;
+  if (g == 0 && tptr_out[n] > n_tgt) tptr_out[n] = n_tgt;
   for (int64_t j = 0; j < cnt; ++j) {
     for (int d = 0; d < 3; ++d) {
       tgt_out[3 * (dst0 + j) + d] = tgt[3 * (src0 + j) + d];
@@ -827,8 +842,7 @@ int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* c
                         const int64_t* tgt_ptr, const double* tgt_xyz, const double* tgt_nrm,
                         int64_t n_tgt, void* workspace, int64_t ws_bytes, double* ctr_out,
                         int64_t* tptr_out, double* tgt_out, double* tnrm_out, int64_t* tgt_index,
-                        void* stream) {
-  (void)n_tgt;
+                        int64_t* bad, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_ctr < 0 || ws_bytes < tsqbx_order_workspace_bytes(n_ctr) || !workspace)
     return set_error(TSQBX_ERR_ARGUMENT, "order_targets: bad sizes or workspace");
@@ -839,11 +853,17 @@ int tsqbx_order_targets(int64_t n_ctr, const int32_t* ctr_order, const double* c
   int64_t* cnt = reinterpret_cast<int64_t*>(ws);
   void* tmp = ws + align256((n_ctr + 1) * sizeof(int64_t));
   size_t tb = (size_t)ws_bytes - align256((n_ctr + 1) * sizeof(int64_t));
-  order_count<<<(int)((n_ctr + 256) / 256), 256, 0, st>>>(ctr_order, tgt_ptr, n_ctr, cnt);
+  if (bad) {
+    const cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int64_t), st);
+    if (e != cudaSuccess) return check_cuda(e, "order_targets memset");
+  }
+  order_count<<<(int)((n_ctr + 256) / 256), 256, 0, st>>>(ctr_order, tgt_ptr, n_ctr, n_tgt, cnt,
+                                                          bad);
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, tptr_out, (int)(n_ctr + 1), st);
   if (n_ctr > 0)
     order_copy<<<(int)((n_ctr + 255) / 256), 256, 0, st>>>(ctr_order, ctr_xyz, tgt_ptr, tgt_xyz,
-                                                            tgt_nrm, n_ctr, tptr_out, ctr_out,
+                                                            tgt_nrm, n_ctr, n_tgt, cnt,
+                                                            tptr_out, ctr_out,
                                                             tgt_out, tnrm_out, tgt_index);
   return check_cuda(cudaGetLastError(), "order_targets launch");
 }

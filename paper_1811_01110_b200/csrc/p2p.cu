@@ -316,19 +316,23 @@ __global__ void p2p_singular_kernel(const double4* __restrict__ sp, int64_t n_sr
 
 __global__ void p2p_set_key(unsigned long long* key, unsigned long long v) { *key = v; }
 
-int g_sms = 0;
+// per-device SM counts (a process may drive several GPUs; B200 has 148)
+static int g_sms[64] = {0};
 
 int sm_count() {
-  if (g_sms == 0) {
-    int dev = 0, n = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
-      g_sms = n;
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 148;      // B200; only reached for size queries without a device
+  }
+  if (g_sms[dev] == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      g_sms[dev] = n;
     else
-      g_sms = 148;   // B200; only reached for size queries without a device
+      g_sms[dev] = 148;
     cudaGetLastError();
   }
-  return g_sms;
+  return g_sms[dev];
 }
 
 int ilog2_ceil(int64_t v) {

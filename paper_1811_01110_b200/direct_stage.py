@@ -54,6 +54,7 @@ def _owner_rows(owned_start, owned_end, cls, n_points, is_target_box):
     return row_start.astype(np.int64), row_box
 
 
+@dv.on_device
 def box_rows(row_box, list_starts, list_flat, box_src_start, box_src_end, device=None):
     """Device CSR (row_ptr int64, row_idx int32) of the concatenated owned source
     ranges of each row's box list (``tsqbx_box_rows_count/fill``)."""
@@ -98,6 +99,7 @@ class DirectStage:
     when ``set_weights`` gave a new density and launch the two kernels.
     """
 
+    @dv.on_device
     def __init__(self, spec: KernelSpec, p_qbx: int, tree, target_boxes, weights,
                  source_normals=None, qtargets=None, qnormals=None, conv_normals=None,
                  device=None):
@@ -134,6 +136,7 @@ class DirectStage:
         self._plans = {}
         self._version = 0
 
+    @dv.on_own_device
     def set_weights(self, weights) -> None:
         """A new (permuted) density for the same tree: sources are repacked lazily."""
         self.weights = dv.to_device(weights, torch.complex128, self.dev, (-1,))
@@ -169,6 +172,7 @@ class DirectStage:
         self._plans[key] = plan
         return plan
 
+    @dv.on_own_device
     def run(self, list_csr):
         """(conv_near, qbx_near_val, ts_pairs): the stage's additions to the
         driver's accumulators (complex128 CUDA tensors over the tree-ordered

@@ -245,6 +245,15 @@ class DeviceGeometry:
         from . import _device as dv
 
         dev = dv.require_cuda(device)
+        with torch.cuda.device(dev):
+            return cls._from_host(disc, centers, dev)
+
+    @classmethod
+    def _from_host(cls, disc, centers, dev):
+        import torch
+
+        from . import _device as dv
+
         put = lambda a: dv.to_device(a, torch.float64, dev)  # noqa: E731
         return cls(nodes=put(disc.nodes), weights=put(disc.weights), normals=put(disc.normals),
                    centers=put(centers.centers), radii=put(centers.radii),
@@ -262,7 +271,8 @@ class DeviceGeometry:
         from . import _device as dv
         from .tsqbx import near_field_potentials
 
-        dens = dv.to_device(density, torch.complex128, self.nodes.device, (-1,))
+        dev = self.nodes.device
+        dens = dv.to_device(density, torch.complex128, dev, (-1,))
         if dens.shape[0] != self.nodes.shape[0]:
             raise ValueError("density must have one value per source node")
         w = self.weights.to(torch.complex128) * dens
@@ -270,4 +280,4 @@ class DeviceGeometry:
         tn = self.target_normals if cfg.spec.needs_target_normals else None
         return near_field_potentials(cfg, self.nodes, w, self.centers, self.radii * near_mult,
                                      self.targets, source_normals=nrm, target_normals=tn,
-                                     validate=validate)
+                                     validate=validate, device=dev)

@@ -48,6 +48,11 @@ class NearLists:
     sell_idx: torch.Tensor | None = None
 
     @property
+    def dev(self) -> torch.device:
+        return self.ptr.device
+
+    @property
+    @dv.on_own_device
     def idx(self) -> torch.Tensor:
         """CSR entries (materialised from the SELL copy on first use: the fast
         kernels read only the SELL layout)."""
@@ -66,6 +71,7 @@ class NearLists:
     def mean_len(self) -> float:
         return self.n_pairs / max(1, self.n_ctr)
 
+    @dv.on_own_device
     def build_sell(self) -> "NearLists":
         """Add the sliced-ELL (SELL-32) copy the thread-per-center kernels read:
         slices of 32 rows, entries column-major (coalesced index loads)."""
@@ -95,12 +101,21 @@ class NearLists:
         return self.n_pairs / max(1, int(self.sell_ptr[-1].item()))
 
     @classmethod
+    @dv.on_device
     def from_user_csr(cls, ptr, idx, n_src: int, device=None) -> "NearLists":
-        dev = dv.require_cuda(device)
+        """A caller's CSR (rows by center, entries index ``sources``), checked the
+        way the reference's indexing would fail: ``ptr[0] == 0``, non-decreasing,
+        ``ptr[-1] == len(idx)``, ``0 <= idx < n_src`` (ValueError otherwise)."""
+        dev = device
         p = dv.to_device(ptr, torch.int64, dev)
         i = dv.to_device(idx, torch.int32, dev)
         n_ctr = int(p.shape[0]) - 1
         n_pairs = int(i.shape[0])
+        if n_ctr < 0:
+            raise ValueError("near-list ptr must have n_centers + 1 entries")
+        check_offsets(p, n_pairs, "near-list ptr")
+        if n_pairs and bool(((i < 0) | (i >= n_src)).any()):
+            raise ValueError(f"near-list indices must lie in [0, {n_src})")
         return cls(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=p, csr_idx=i)
 
     def to_user_csr(self) -> tuple[np.ndarray, np.ndarray]:
@@ -123,9 +138,21 @@ class NearLists:
         return uptr, uidx.astype(np.int32)
 
 
+def check_offsets(ptr: torch.Tensor, total: int, name: str) -> None:
+    """CSR offsets: ptr[0] == 0, non-decreasing, ptr[-1] == total (one read-back);
+    malformed offsets would otherwise index outside the device arrays."""
+    if ptr.numel() == 0:
+        raise ValueError(f"{name} must not be empty")
+    ends = torch.stack([ptr[0], ptr[-1], (ptr[1:] < ptr[:-1]).any().to(torch.int64)]).tolist()
+    if ends[0] != 0 or ends[1] != total or ends[2]:
+        raise ValueError(f"{name} must start at 0, be non-decreasing and end at {total} "
+                         f"(got first {ends[0]}, last {ends[1]})")
+
+
 _BOUND_BYTES_MAX = 16 << 30     # bound-sized SELL buffer above this: count exactly
 
 
+@dv.on_device
 def build_near_lists(centers, sources, radii, device=None, sell: bool = True) -> NearLists:
     """Radius-ball near lists {s : |s - c|^2 <= rad_c^2} on the device.
 

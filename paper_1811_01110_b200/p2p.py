@@ -41,6 +41,7 @@ class P2PProblem:
     """Sources packed once in HBM; evaluate dense or row-restricted sums against
     any set of targets (repeated evaluations reuse the packed sources)."""
 
+    @dv.on_device
     def __init__(self, spec: KernelSpec, sources, weights, source_normals=None, device=None):
         self.spec = spec
         self.dev = dv.require_cuda(device)
@@ -70,6 +71,7 @@ class P2PProblem:
                                         dv.ptr(self.sn), None, self.packed.data_ptr(),
                                         dv.stream_handle(self.dev)), "tsqbx_pack_sources")
 
+    @dv.on_own_device
     def set_weights(self, weights) -> None:
         """New source weights (same sources): one pack kernel, no reallocation."""
         if isinstance(weights, torch.Tensor) and not weights.is_complex():
@@ -79,6 +81,7 @@ class P2PProblem:
             raise ValueError("weights must have one entry per source")
         self._pack(w)
 
+    @dv.on_own_device
     def rows(self, row_tgt, row_ptr, row_idx, n_tgt: int) -> "P2PRows":
         """Checked device copy of a row structure for repeated ``evaluate``."""
         rt = dv.to_device(row_tgt, torch.int64, self.dev, (-1,))
@@ -106,6 +109,7 @@ class P2PProblem:
                 raise ValueError("target normals must have one entry per target")
         return tgt, tn
 
+    @dv.on_own_device
     def evaluate(self, targets, target_normals=None, rows=None, validate: bool = True,
                  out: torch.Tensor | None = None) -> torch.Tensor:
         """complex128 (n_tgt,) CUDA tensor.  ``rows = (row_tgt, row_ptr, row_idx)``
@@ -156,6 +160,7 @@ def _host_out(sources) -> bool:
     return not (isinstance(sources, torch.Tensor) and sources.is_cuda)
 
 
+@dv.on_device
 def direct_sum(spec: KernelSpec, sources, weights, targets, source_normals=None,
                target_normals=None, device=None):
     """sum_j w_j K(x_i, y_j) for every target (kernels.py:114-136) on the GPU.
@@ -198,6 +203,7 @@ def kernel_value(spec: KernelSpec, target, source, target_normal=None,
     return complex(out[0])
 
 
+@dv.on_device
 def p2p_rows(spec: KernelSpec, sources, weights, targets, row_tgt, row_ptr, row_idx,
              source_normals=None, target_normals=None, device=None):
     """Batched per-box p2p (driver.py:187-210): row r's targets see only the

@@ -98,7 +98,7 @@ class _Prepared:
     """
 
     def __init__(self, cfg: TsConfig, dev, src, w, sn, ctr, near: NearLists, tgt, tn, tptr,
-                 group_lanes=None):
+                 group_lanes=None, user_tptr: bool = True):
         L = _lib.load()
         self.cfg, self.dev, self.near = cfg, dev, near
         self.src, self.w, self.sn = src, w, sn
@@ -110,6 +110,16 @@ class _Prepared:
             raise ValueError(f"near lists have {near.n_ctr} rows for {self.n_ctr} centers")
         if int(tptr.shape[0]) != self.n_ctr + 1:
             raise ValueError("tgt_ptr must have n_centers + 1 entries")
+        # err[0]: the evaluation's validation key; err[1]: 1 when a caller's
+        # tgt_ptr is malformed (checked on the device by tsqbx_order_targets,
+        # reported with the result: no extra synchronisation)
+        self.err = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.check_tptr = False
+        if user_tptr and near.ctr_order is None:
+            # rows in the caller's order (a user CSR, already checked with one
+            # read-back): check the target offsets the same way
+            from .nearlist import check_offsets
+            check_offsets(tptr, self.n_tgt, "tgt_ptr")
         spec = cfg.spec
         self.eq = _equation_code(spec)
         self.variant = spec.variant_code
@@ -135,11 +145,13 @@ class _Prepared:
                                              dv.ptr(tn), self.n_tgt, ws.data_ptr(), wsb,
                                              self.ctr.data_ptr(), self.tptr.data_ptr(),
                                              self.tgt.data_ptr(), dv.ptr(self.tn),
-                                             self.tidx.data_ptr(), st), "tsqbx_order_targets")
+                                             self.tidx.data_ptr(),
+                                             self.err[1:].data_ptr() if user_tptr else None, st),
+                       "tsqbx_order_targets")
+            self.check_tptr = user_tptr
         self.ws_bytes = int(L.tsqbx_eval_workspace_bytes(self.eq, self.variant, cfg.p_qbx,
                                                          self.n_tgt))
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
-        self.err = torch.empty(1, dtype=torch.int64, device=dev)
         self.layout = "csr" if group_lanes else pick_layout()
         if group_lanes:
             self.G = int(group_lanes)
@@ -226,9 +238,18 @@ class _Prepared:
             dv.stream_handle(self.dev)), "tsqbx_eval_packed")
 
     # --- validation -----------------------------------------------------------
+    def raise_bad_tptr(self) -> None:
+        raise ValueError(f"tgt_ptr must start at 0, be non-decreasing and end at {self.n_tgt}")
+
+    def check_inputs(self) -> None:
+        """Raise if the device check of the caller's tgt_ptr failed (one read-back)."""
+        if self.check_tptr and int(self.err[1].item()):
+            self.raise_bad_tptr()
+
     def check_errors(self, batch_context: bool) -> None:
         """Raise the reference's ValueError if the screened launch flagged a pair."""
-        if int(self.err.item()) == _lib.ERR_KEY_NONE:
+        self.check_inputs()
+        if int(self.err[0].item()) == _lib.ERR_KEY_NONE:
             return
         L = _lib.load()
         near = self.near
@@ -237,7 +258,7 @@ class _Prepared:
                                     self.tgt.data_ptr(), self.tptr.data_ptr(), self.n_tgt,
                                     self.err.data_ptr(), dv.stream_handle(self.dev)),
                    "tsqbx_validate")
-        key = int(self.err.item())
+        key = int(self.err[0].item())
         if key == _lib.ERR_KEY_NONE:
             return            # screen tripped on non-finite weights, not on geometry
         tp, kind, pos = key >> 32, (key >> 31) & 1, key & 0x7FFFFFFF
@@ -292,8 +313,9 @@ class PendingPotentials:
     def __init__(self, prep, res: torch.Tensor, out, host_out: bool, validate: bool):
         self._prep, self._res = prep, res
         self._err = None
-        if validate and prep.n_tgt:
-            self._err = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        self._validate = validate
+        if (validate and prep.n_tgt) or prep.check_tptr:
+            self._err = torch.empty(2, dtype=torch.int64, pin_memory=True)
             self._err.copy_(prep.err, non_blocking=True)
         self._numpy = out is None and host_out
         if self._numpy:
@@ -312,13 +334,17 @@ class PendingPotentials:
 
     def result(self):
         self._event.synchronize()
-        if self._err is not None and int(self._err[0]) != _lib.ERR_KEY_NONE:
-            self._prep.check_errors(batch_context=True)
+        if self._err is not None:
+            if self._prep.check_tptr and int(self._err[1]):
+                self._prep.raise_bad_tptr()
+            if self._validate and int(self._err[0]) != _lib.ERR_KEY_NONE:
+                self._prep.check_errors(batch_context=True)
         if self._out is None:
             return self._res
         return self._out.numpy() if self._numpy else self._out
 
 
+@dv.on_device
 def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
                         tgt_ptr=None, source_normals=None, target_normals=None,
                         validate: bool = True, group_lanes: int | None = None, device=None,
@@ -354,7 +380,8 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
     if not isinstance(near, NearLists):
         nptr, nidx = near
         near = NearLists.from_user_csr(nptr, nidx, int(src.shape[0]), dev)
-    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes,
+                     user_tptr=tgt_ptr is not None)
     if tgt_ptr is None:
         prep.set_uniform_targets(known=True)
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
@@ -368,6 +395,8 @@ def ts_accumulate_batch(cfg: TsConfig, sources, weights, centers, targets, near,
         return pend if not sync else pend.result()
     if prep.n_tgt and validate:
         prep.check_errors(batch_context=True)
+    else:
+        prep.check_inputs()
     return _deliver(res, out, host_out)
 
 
@@ -383,6 +412,7 @@ def _deliver(out_dev: torch.Tensor, out, host_out: bool):
     return out_dev.cpu().numpy() if host_out else out_dev
 
 
+@dv.on_device
 def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, targets,
                           tgt_ptr=None, source_normals=None, target_normals=None,
                           validate: bool = True, group_lanes: int | None = None, device=None,
@@ -420,14 +450,19 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
     for t in (w, tgt, sn, tn, tptr):
         if t is not None:
             t.record_stream(main)
-    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+    if tgt_ptr is None and int(tgt.shape[0]) != n_ctr:
+        raise ValueError("tgt_ptr is required unless there is one target per center")
+    prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes,
+                     user_tptr=tgt_ptr is not None)
     if tgt_ptr is None:
         prep.set_uniform_targets(known=True)
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
         prep.launch(torch.view_as_real(res), validate)
-        if validate:
-            prep.check_errors(batch_context=True)
+    if prep.n_tgt and validate:
+        prep.check_errors(batch_context=True)
+    else:
+        prep.check_inputs()
     return _deliver(res, out, host_out)
 
 
@@ -438,6 +473,7 @@ class TsqbxProblem:
     nothing is copied between host and device.
     """
 
+    @dv.on_device
     def __init__(self, cfg: TsConfig, sources, weights, centers, targets, near: NearLists,
                  tgt_ptr=None, source_normals=None, target_normals=None,
                  group_lanes: int | None = None, device=None):
@@ -445,13 +481,22 @@ class TsqbxProblem:
         src, w, ctr, tgt, sn, tn = _inputs(cfg, sources, weights, centers, targets,
                                            source_normals, target_normals, dev)
         n_ctr = int(ctr.shape[0])
+        if tgt_ptr is None and int(tgt.shape[0]) != n_ctr:
+            raise ValueError("tgt_ptr is required unless there is one target per center")
         tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
                 else dv.to_device(tgt_ptr, torch.int64, dev))
-        self.prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes)
+        self.prep = _Prepared(cfg, dev, src, w, sn, ctr, near, tgt, tn, tptr, group_lanes,
+                              user_tptr=tgt_ptr is not None)
+        self.prep.check_inputs()        # once per problem (evaluate() never re-checks)
         self.prep.set_uniform_targets(known=tgt_ptr is None)
         self.out = torch.empty(self.prep.n_tgt, dtype=torch.complex128, device=dev)
         self.n_pairs_per_target = None
 
+    @property
+    def dev(self) -> torch.device:
+        return self.prep.dev
+
+    @dv.on_own_device
     def set_weights(self, weights) -> None:
         """New densities for the same geometry (GMRES matvecs): one pack kernel."""
         if isinstance(weights, torch.Tensor) and not weights.is_complex():
@@ -467,6 +512,7 @@ class TsqbxProblem:
     def layout(self) -> str:
         return self.prep.layout
 
+    @dv.on_own_device
     def evaluate(self, validate: bool = False, generic: bool = False) -> torch.Tensor:
         if self.prep.n_tgt:
             self.prep.launch(torch.view_as_real(self.out), validate, generic)
