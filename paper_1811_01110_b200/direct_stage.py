@@ -104,7 +104,7 @@ class DirectStage:
                  source_normals=None, qtargets=None, qnormals=None, conv_normals=None,
                  device=None):
         self.dev = dv.require_cuda(device)
-        self.spec = spec
+        spec = self.spec = KernelSpec.coerce(spec)
         self.cfg = TsConfig(spec, int(p_qbx))
         dev = self.dev
         self.sources = dv.to_device(tree.points[SOURCES], torch.float64, dev, (-1, 3))

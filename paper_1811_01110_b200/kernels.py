@@ -49,6 +49,16 @@ class KernelSpec:
         elif self.helmholtz_k is not None:
             raise ValueError("helmholtz_k only valid for the Helmholtz equation")
 
+    @classmethod
+    def coerce(cls, spec) -> "KernelSpec":
+        """This type from any spec with the reference's fields (e.g. a
+        ``gigaqbx.kernels.KernelSpec`` handed over by the reference's driver):
+        equal enum values, the same ``helmholtz_k``."""
+        if isinstance(spec, cls):
+            return spec
+        return cls(equation=Equation(spec.equation.value), variant=Variant(spec.variant.value),
+                   helmholtz_k=spec.helmholtz_k)
+
     @property
     def is_laplace(self) -> bool:
         return self.equation is Equation.LAPLACE

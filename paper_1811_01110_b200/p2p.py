@@ -43,7 +43,7 @@ class P2PProblem:
 
     @dv.on_device
     def __init__(self, spec: KernelSpec, sources, weights, source_normals=None, device=None):
-        self.spec = spec
+        spec = self.spec = KernelSpec.coerce(spec)
         self.dev = dv.require_cuda(device)
         L = _lib.load()
         src = dv.to_device(sources, torch.float64, self.dev, (-1, 3))

@@ -44,6 +44,7 @@ class TsConfig:
     p_qbx: int
 
     def __post_init__(self):
+        object.__setattr__(self, "spec", KernelSpec.coerce(self.spec))
         if self.p_qbx < 0:
             raise ValueError("p_qbx must be nonnegative")
 

@@ -66,3 +66,24 @@ def test_kernel_value_checks_before_the_gpu():
     with pytest.raises(ValueError, match="source normal must be unit length"):
         kernel_value(KernelSpec(variant=Variant.SOURCE_NORMAL_DERIV), np.array([1.0, 0, 0]),
                      np.zeros(3), source_normal=np.array([0.0, 0, 2.0]))
+
+
+def test_kernel_spec_coerce_from_foreign_spec():
+    # the reference driver hands its own KernelSpec type to DirectStage / TsConfig
+    import enum
+    from types import SimpleNamespace
+
+    from paper_1811_01110_b200.kernels import Equation, KernelSpec, Variant
+
+    class Eq(enum.Enum):
+        HELMHOLTZ = "helmholtz"
+
+    class Va(enum.Enum):
+        D = "d"
+
+    foreign = SimpleNamespace(equation=Eq.HELMHOLTZ, variant=Va.D, helmholtz_k=2.5)
+    spec = KernelSpec.coerce(foreign)
+    assert spec == KernelSpec(Equation.HELMHOLTZ, Variant.SOURCE_NORMAL_DERIV, 2.5)
+    assert KernelSpec.coerce(spec) is spec
+    from paper_1811_01110_b200 import TsConfig
+    assert TsConfig(foreign, 4).spec == spec
