@@ -731,26 +731,43 @@ def main_ours(args):
 
 
 def main_distributed(torch, args, case, dev, flush, rank, world, local):
-    """N ranks, one GPU each.  Default (`--scaling weak`, the tier rule for a
-    path that partitions): every rank owns an independent problem of the N=1
-    size (same configuration, seed = rank) and evaluates it with no data-path
-    collective; the step time is the max over ranks (device events, all-reduced
-    after the timed region) and `value` = all ranks' pairs / that time.
-    `--scaling strong`: one problem split by pair count over the ranks plus one
-    NCCL all-gather of the potentials per step (`ShardedEvaluator`)."""
+    """N ranks, one GPU each (torchrun; NCCL process group).
+
+    Default (`--scaling strong`, north_star): ONE problem -- the N=1 workload --
+    split over the ranks by `ShardedProblem` (centers in Morton order cut into
+    equal-pair ranges, each rank building only its own near lists, sources
+    replicated; per step: the rank's rows in chunks with the all-gather of
+    chunk c overlapping chunk c+1, then one scatter into user order on every
+    rank).  The step time is the max over ranks of the device-event time
+    (all-reduced after the timed region); `value` = the problem's pairs / that
+    time.  `--scaling weak`: an independent problem of the N=1 size per rank
+    (seed = rank), no data-path collective; `value` = all ranks' pairs / time.
+    Run with NCCL_DEBUG=INFO to see the transport (NVLink / NVLS) NCCL chose."""
     import torch.distributed as dist
     from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs
-    from paper_1811_01110_b200.distributed import ShardedEvaluator
+    from paper_1811_01110_b200.distributed import ShardedProblem
 
     dist.init_process_group("nccl", device_id=dev)
     weak = args.scaling == "weak"
     if weak:
         case = configs.make_case(args.case, args.preset, seed=rank)
-    near = build_near_lists(case.centers, case.sources, case.near_radii, dev)
-    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
-                        tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev)
-    pairs = prob.pair_count()
-    step = prob.evaluate if weak else ShardedEvaluator(prob, rank, world).evaluate
+        near = build_near_lists(case.centers, case.sources, case.near_radii, dev)
+        prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                            near, tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None,
+                            device=dev)
+        pairs = prob.pair_count()
+        step = prob.evaluate
+        chunks = None
+    else:
+        t_setup = time.perf_counter()
+        prob = ShardedProblem(case.cfg, case.sources, case.weights, case.centers, case.targets,
+                              case.near_radii, tgt_ptr=case.tgt_ptr, rank=rank, world=world,
+                              chunks=args.chunks, device=dev)
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter() - t_setup
+        pairs = prob.n_pairs_rank
+        step = prob.evaluate
+        chunks = prob.layout.chunks
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -758,7 +775,7 @@ def main_distributed(torch, args, case, dev, flush, rank, world, local):
     with sampler:
         t_end = time.perf_counter() + args.soak_seconds
         while time.perf_counter() < t_end:     # soak: clocks settle under this load
-            for _ in range(20):
+            for _ in range(5):
                 step()
             torch.cuda.synchronize()
         dist.barrier()
@@ -773,16 +790,49 @@ def main_distributed(torch, args, case, dev, flush, rank, world, local):
     tot_pairs = stats[1:].clone()
     dist.all_reduce(tot_pairs, op=dist.ReduceOp.SUM)
     e2e = None
-    if weak and not args.no_e2e:
-        r = measure_e2e(torch, case, args, dev)
-        e_ms = torch.tensor([sum(r["ms"]) / len(r["ms"])], dtype=torch.float64, device=dev)
+    if not args.no_e2e:
+        if weak:
+            r = measure_e2e(torch, case, args, dev)
+            e_ms_local = sum(r["ms"]) / len(r["ms"])
+            h2d, d2h = r["h2d"] * world, r["d2h"] * world
+            path = "ts_accumulate_batch on every rank (pinned host in/out), max over ranks"
+        else:
+            # solver matvec through the sharded problem: every step a new
+            # density H2D (pinned, replicated), the sharded evaluation with its
+            # all-gather, and the full potential vector D2H on every rank
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa
+            dens = [pin(case.weights * (1.0 + 0.1 * i)) for i in range(2)]
+            hout = torch.empty(case.n_targets, dtype=torch.complex128).pin_memory()
+
+            def matvec(i=[0]):  # noqa: B006
+                prob.set_weights(dens[i[0] % 2])
+                i[0] += 1
+                hout.copy_(step(), non_blocking=True)
+            for _ in range(3):
+                matvec()
+            torch.cuda.synchronize()
+            dist.barrier()
+            mms = []
+            for _ in range(max(1, args.steps)):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                matvec()
+                e1.record()
+                e1.synchronize()
+                mms.append(e0.elapsed_time(e1))
+            e_ms_local = sum(mms) / len(mms)
+            h2d, d2h = case.n_sources * 16 * world, case.n_targets * 16 * world
+            path = ("ShardedProblem.set_weights(pinned density, every rank) -> sharded "
+                    "evaluation + NCCL all-gather -> D2H of all potentials on every rank; "
+                    "geometry and each rank's near lists resident")
+        e_ms = torch.tensor([e_ms_local], dtype=torch.float64, device=dev)
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(tot_pairs.item()) / (float(e_ms.item()) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": r["h2d"] * world, "d2h_bytes_per_step": r["d2h"] * world,
-               "ms_per_step": float(e_ms.item()),
-               "path": "ts_accumulate_batch on every rank (pinned host in/out), max over ranks"}
+        step_pairs_e = float(tot_pairs.item())
+        e2e = {"value": step_pairs_e / (float(e_ms.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(e_ms.item()), "path": path}
     t = float(tmax.item())
-    step_pairs = float(tot_pairs.item()) if weak else float(pairs)
+    step_pairs = float(tot_pairs.item())
     if rank == 0:
         fpp = configs.algorithmic_flops_per_pair(case.cfg.spec, case.cfg.p_qbx)
         per_gpu_tf = step_pairs * fpp / (t / args.steps * 1e-3) / 1e12 / world
@@ -791,24 +841,24 @@ def main_distributed(torch, args, case, dev, flush, rank, world, local):
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": t / args.steps, "higher_is_better": True,
                 "scaling": "weak" if weak else "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload_name(case), "case": case.name,
-                           "preset": case.preset, "pairs_per_step": step_pairs,
-                           "l2": "flushed between steps (256 MB write, outside the timed events)",
-                           "parallelism": (f"{world} independent problems (seed = rank), one per "
-                                           "GPU, no data-path collective" if weak else
-                                           f"centers sharded by pair count over {world} ranks, "
-                                           "sources replicated, 1 NCCL all-gather per step")},
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, BASELINE.json configuration geometry)",
+                "config": bench_config(case, args),
+                "workload_stats": {"pairs_per_step": step_pairs,
+                                   "all_gather_chunks": chunks,
+                                   "setup_s_rank0": None if weak else round(t_setup, 3)},
                 "roofline": {"bound": "fp64", "achieved": per_gpu_tf, "unit": "TFLOP/s per GPU",
                              "peak": peak, "frac": per_gpu_tf / peak if peak else None,
                              "traffic": None},
-                "gpu_launches": (1 if weak else 2) * args.steps,
+                "gpu_launches": (1 if weak else 1 + (chunks or 1)) * args.steps,
                 "clocks": clocks}
         if e2e:
             line["e2e"] = e2e
         print(json.dumps(line))
     dist.destroy_process_group()
     return 0
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 7
+#define TSQBX_ABI_VERSION 8
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -98,6 +98,11 @@ int tsqbx_pack_sources(int64_t n_src, const double* xyz, const double* w, const 
  *   tgt_nrm     : n_tgt x 3 (S' only, else NULL)
  *   tgt_out     : output slot of each target (NULL = identity); the value of
  *                 target t is written to out[(tgt_out ? tgt_out[t] : t) - out_offset]
+ *   tgt_base    : with TSQBX_FLAG_UNIFORM_TARGETS (k = flags >> 8 & 255), row g
+ *                 of the launch owns targets tgt_base + k g .. tgt_base + k g + k - 1
+ *                 (no tgt_ptr load; a row range [g0, g1) passes k * g0); the
+ *                 kernels that do not use the uniform form read tgt_ptr, so
+ *                 tgt_ptr must hold the same runs; n_tgt >= tgt_base + k n_ctr
  *   out         : complex128 potentials
  *   err_key     : device int64 (see above); may be NULL when flags lacks VALIDATE
  *   group_lanes : CSR kernels: lanes per center (power of two <= 32, 0 = 8);
@@ -116,8 +121,8 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p,
                       const int64_t* sell_ptr, const int32_t* sell_idx,
                       const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
                       int64_t n_tgt, const int64_t* tgt_out, int64_t out_offset,
-                      unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
-                      double* out, int64_t* err_key, void* stream);
+                      int64_t tgt_base, unsigned flags, int group_lanes, void* workspace,
+                      int64_t ws_bytes, double* out, int64_t* err_key, void* stream);
 
 /* Convenience forms with the reference's names: raw user-layout sources
  * (xyz n x 3, complex weights, optional normals), user-order CSR.  They pack
@@ -189,6 +194,18 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                     const int32_t* ctr_order, int64_t* near_ptr, int32_t* near_idx,
                     const int64_t* sell_ptr, int32_t* sell_idx, int64_t* totals,
                     void* stream);
+/* Rows g0..g1-1 of the processing order only (a rank's shard),
+ * SELL mode: after tsqbx_near_count over ALL centers (CSR mode: exact row
+ * lengths), the caller sizes the shard's slices from near_ptr[g0..g1] (e.g.
+ * tsqbx_sell_size on the rebased offsets) and this call writes the shard's
+ * rows into them, its exact offsets into near_ptr (g1 - g0 + 1 entries, from
+ * 0) and its pair count into totals[0].  g0 must be a multiple of 32. */
+int tsqbx_near_fill_rows(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                         const double* src_xyz, int64_t n_src,
+                         void* workspace, int64_t ws_bytes,
+                         const int32_t* ctr_order, int64_t g0, int64_t g1, int64_t* near_ptr,
+                         const int64_t* sell_ptr, int32_t* sell_idx, int64_t* totals,
+                         void* stream);
 
 /* Reorder centers and their targets into the processing order `ctr_order`
  * (user center ctr_order[g] becomes row g): writes ctr_out (n_ctr x 3),

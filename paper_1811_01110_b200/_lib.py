@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
                                                                "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
-ABI_VERSION = 7      # TSQBX_ABI_VERSION in include/tsqbx.h
+ABI_VERSION = 8      # TSQBX_ABI_VERSION in include/tsqbx.h
 
 # status codes (include/tsqbx.h)
 OK = 0
@@ -54,7 +54,7 @@ SIGNATURES = {
     "tsqbx_pack_sources": (_I, [_I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_eval_workspace_bytes": (_I64, [_I, _I, _I, _I64]),
     "tsqbx_eval_packed": (_I, [_I, _I, _D, _I, _P, _I64, _I, _P, _I64, _P, _P, _P, _P, _P, _P,
-                               _P, _I64, _P, _I64, _U, _I, _P, _I64, _P, _P, _P]),
+                               _P, _I64, _P, _I64, _I64, _U, _I, _P, _I64, _P, _P, _P]),
     "tsqbx_user_workspace_bytes": (_I64, [_I, _I, _I, _I64, _I64]),
     "tsqbx_eval_laplace": (_I, [_I, _I, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64, _U,
                                 _P, _I64, _P, _P, _P]),
@@ -73,6 +73,8 @@ SIGNATURES = {
     "tsqbx_near_workspace_bytes": (_I64, [_I64, _I64]),
     "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "tsqbx_near_fill_rows": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P,
+                                  _P, _P]),
     "tsqbx_fp64_probe": (_I, [_P, _I64, _I, _I, _P]),
     "tsqbx_one_staging_doubles": (_I64, [_I64, _I]),
     "tsqbx_eval_one": (_I, [_I, _I, _D, _I, _P, _I64, _U, _P, _I64, _P, _P]),

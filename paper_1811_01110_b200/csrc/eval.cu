@@ -550,9 +550,9 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
                       const int64_t* near_ptr, const int32_t* near_idx,
                       const int64_t* sell_ptr, const int32_t* sell_idx, const double* tgt_xyz,
                       const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
-                      const int64_t* tgt_out, int64_t out_offset, unsigned flags,
-                      int group_lanes, void* workspace, int64_t ws_bytes, double* out,
-                      int64_t* err_key, void* stream) {
+                      const int64_t* tgt_out, int64_t out_offset, int64_t tgt_base,
+                      unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
+                      double* out, int64_t* err_key, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (equation != TSQBX_EQ_LAPLACE && equation != TSQBX_EQ_HELMHOLTZ)
     return set_error(TSQBX_ERR_ARGUMENT, "bad equation %d", equation);
@@ -598,9 +598,11 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   a.real_w = (flags & TSQBX_FLAG_REAL_WEIGHTS) ? 1 : 0;
   if (flags & TSQBX_FLAG_UNIFORM_TARGETS) {
     a.tuni = (int)((flags >> 8) & 0xffu);
-    if (a.tuni < 1 || n_tgt != (int64_t)a.tuni * n_ctr)
-      return set_error(TSQBX_ERR_ARGUMENT, "uniform targets: n_tgt must be k * n_ctr, 1 <= k <= 255");
+    if (a.tuni < 1 || tgt_base < 0 || tgt_base + (int64_t)a.tuni * n_ctr > n_tgt)
+      return set_error(TSQBX_ERR_ARGUMENT,
+                       "uniform targets: 1 <= k <= 255 and tgt_base + k * n_ctr <= n_tgt");
   }
+  a.tbase = tgt_base;
   a.tgt = tgt_xyz;
   a.tnrm = tgt_nrm;
   a.tptr = tgt_ptr;
@@ -627,7 +629,12 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
           ctr_xyz, n_ctr, tgt_xyz, tgt_ptr, p, k, fast ? 0 : 1, static_cast<double*>(workspace),
           a.ttab_stride);
   }
-  const int nt = (n_tgt >= 2 * n_ctr && !(flags & TSQBX_FLAG_ONE_TARGET)) ? 2 : 1;
+  // targets per row the kernels share source work between: the uniform run
+  // length, else a guess from the totals (a row range of a bigger problem
+  // with a tptr is ambiguous; both choices are correct)
+  const int nt = (flags & TSQBX_FLAG_ONE_TARGET) ? 1
+                 : (flags & TSQBX_FLAG_UNIFORM_TARGETS) ? (a.tuni >= 2 ? 2 : 1)
+                 : (n_tgt >= 2 * n_ctr ? 2 : 1);
   if (fast) {
     (equation == TSQBX_EQ_LAPLACE ? launch_laplace_fast : launch_helmholtz_fast)(
         p, sell_ptr != nullptr, nt, val, a, n_ctr, st);
@@ -665,7 +672,7 @@ static int eval_user(int equation, int variant, double k, int p, const double* s
   if (rc) return rc;
   return tsqbx_eval_packed(equation, variant, k, p, packed, n_src, variant == 2, ctr_xyz, n_ctr,
                            near_ptr, near_idx, nullptr, nullptr, tgt_xyz, tgt_nrm, tgt_ptr,
-                           n_tgt, nullptr, 0,
+                           n_tgt, nullptr, 0, 0,
                            flags, 0, static_cast<char*>(workspace) + pbytes, ws_bytes - pbytes,
                            out, err_key, stream);
 }

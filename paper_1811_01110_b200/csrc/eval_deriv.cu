@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_DERIV_MINB) laplace_deri
   const bool realw = a.real_w || *a.imag_flag == 0u;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = UNI > 0 ? g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
+  const int64_t t0 = UNI > 0 ? a.tbase + g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], rr[NT], ir[NT], nx[NT], ny[NT], nz[NT], ntt[NT];
     double ar[NT], ai[NT];
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kSellBlock, VARIANT == 2 ? 2 : 1) helmholtz_de
   const bool val = a.validate != 0;
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = UNI > 0 ? g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
+  const int64_t t0 = UNI > 0 ? a.tbase + g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], nx[NT], ny[NT], nz[NT], ntt[NT];

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
   if (g < a.n_ctr) {
   const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
   const int len = (int)(a.nptr[g + 1] - a.nptr[g]);
-  const int64_t t0 = UNI > 0 ? g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
+  const int64_t t0 = UNI > 0 ? a.tbase + g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
   const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];

@@ -24,6 +24,7 @@ struct EvalParams {
   const double* __restrict__ ttab;   // Helmholtz per-target Bessel table
   double2* __restrict__ out;
   int64_t out_offset;
+  int64_t tbase;                     // uniform runs: target index of the launch's row 0
   unsigned long long* err;
   int64_t n_ctr;
   int ttab_stride;
@@ -274,7 +275,7 @@ __device__ __forceinline__ RowHead load_head(const EvalParams& a, int64_t g) {
   h.soff = a.sell_ptr[g >> 5];
   h.len = (int)(a.nptr[g + 1] - a.nptr[g]);
   if (UNI > 0) {       // uniform target runs: the target range needs no load
-    h.t0 = g * UNI;
+    h.t0 = a.tbase + g * UNI;
     h.t1 = h.t0 + UNI;
   } else {
     h.t0 = a.tptr[g];

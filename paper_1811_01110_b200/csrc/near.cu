@@ -830,6 +830,43 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
   return check_cuda(cudaGetLastError(), "near_fill launch");
 }
 
+int tsqbx_near_fill_rows(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                         const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
+                         const int32_t* ctr_order, int64_t g0, int64_t g1, int64_t* near_ptr,
+                         const int64_t* sell_ptr, int32_t* sell_idx, int64_t* totals,
+                         void* stream) {
+  (void)src_xyz;
+  cudaStream_t st = (cudaStream_t)stream;
+  const NearLayout L = near_layout(n_ctr, n_src);
+  if (!workspace || ws_bytes < (int64_t)L.total)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_fill_rows: workspace too small");
+  if (g0 < 0 || g1 < g0 || g1 > n_ctr || (g0 & 31) || !near_ptr || !sell_ptr || !sell_idx ||
+      !totals || (g1 > g0 && (!ctr_xyz || !radius || !ctr_order)))
+    return set_error(TSQBX_ERR_ARGUMENT,
+                     "near_fill_rows: bad row range (g0 must be a multiple of 32) or null array");
+  char* ws = static_cast<char*>(workspace);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
+  const int64_t n = g1 - g0;
+  // rows g0..g1 of the processing order (a rank's shard): the same sweep as
+  // tsqbx_near_fill with the row index shifted, the source grid and hash of
+  // tsqbx_near_count shared by all ranges
+  if (n > 0)
+    sweep_cell_kernel<1><<<(int)((n + 127) / 128), 128, 0, st>>>(
+        ctr_xyz, radius, n, ctr_order + g0, reinterpret_cast<const double*>(ws + L.off_prm),
+        reinterpret_cast<const double4*>(ws + L.off_sxyz),
+        reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
+        reinterpret_cast<const int32_t*>(ws + L.off_hst),
+        reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, cnt, near_ptr, nullptr,
+        sell_ptr, sell_idx);
+  set_tail<<<1, 1, 0, st>>>(cnt, n);
+  size_t tb = L.tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(ws + L.off_tmp, tb, cnt, near_ptr, (int)(n + 1), st);
+  const cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n, sizeof(int64_t),
+                                        cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "near_fill_rows copy");
+  return check_cuda(cudaGetLastError(), "near_fill_rows launch");
+}
+
 int64_t tsqbx_order_workspace_bytes(int64_t n_ctr) {
   if (n_ctr < 0) return -1;
   size_t t = 0;

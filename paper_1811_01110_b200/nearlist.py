@@ -234,3 +234,78 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
                      csr_idx=None if idx is None else idx[:n_pairs],
                      src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],
                      sell_ptr=sptr, sell_idx=sidx)
+
+
+class NearRowBuilder:
+    """Near lists built one processing-row range at a time (multi-GPU shards).
+
+    ``tsqbx_near_count`` runs once over ALL centers (Morton sort of sources and
+    centers, source grid/hash, exact row lengths): every rank knows the global
+    processing order and every row's length, so it can cut the rows into
+    ranges of equal pair count; ``rows(g0, g1)`` then fills only that range's
+    lists (``tsqbx_near_fill_rows``, SELL-32x4) -- a rank never stores the
+    other ranks' indices.
+    """
+
+    @dv.on_device
+    def __init__(self, centers, sources, radii, device=None):
+        self.dev = dev = device
+        L = _lib.load()
+        self.ctr = dv.to_device(centers, torch.float64, dev, (-1, 3))
+        self.src = dv.to_device(sources, torch.float64, dev, (-1, 3))
+        self.n_ctr, self.n_src = int(self.ctr.shape[0]), int(self.src.shape[0])
+        if isinstance(radii, torch.Tensor):
+            rad = radii.to(device=dev, dtype=torch.float64).reshape(-1).contiguous()
+            self.rad = rad.expand(self.n_ctr).contiguous() if rad.numel() == 1 else rad
+        else:
+            self.rad = dv.to_device(np.broadcast_to(np.asarray(radii, dtype=np.float64),
+                                                    (self.n_ctr,)), torch.float64, dev)
+        st = dv.stream_handle(dev)
+        self.ws_bytes = int(L.tsqbx_near_workspace_bytes(self.n_ctr, self.n_src))
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
+        self.src_perm = torch.empty(max(self.n_src, 1), dtype=torch.int32, device=dev)
+        self.ctr_order = torch.empty(max(self.n_ctr, 1), dtype=torch.int32, device=dev)
+        self.ptr = torch.empty(self.n_ctr + 1, dtype=torch.int64, device=dev)
+        self.totals = torch.zeros(2, dtype=torch.int64, device=dev)
+        _lib.check(L.tsqbx_near_count(self.ctr.data_ptr(), self.rad.data_ptr(), self.n_ctr,
+                                      self.src.data_ptr(), self.n_src, self.ws.data_ptr(),
+                                      self.ws_bytes, self.src_perm.data_ptr(),
+                                      self.ctr_order.data_ptr(), self.ptr.data_ptr(), None,
+                                      self.totals.data_ptr(), st), "tsqbx_near_count")
+        self.n_pairs = int(self.totals[0].item())
+
+    @property
+    def row_lengths(self) -> torch.Tensor:
+        """Exact near-list length of every processing row (device int64)."""
+        return self.ptr[1:self.n_ctr + 1] - self.ptr[:self.n_ctr]
+
+    @dv.on_own_device
+    def rows(self, g0: int, g1: int) -> NearLists:
+        """The lists of processing rows [g0, g1) (g0 a multiple of 32) as a
+        NearLists in that range's order (row i = processing row g0 + i; its user
+        center is ``ctr_order[g0 + i]``), indices into the packed (Morton)
+        source order shared by all ranges."""
+        if g0 % 32 or not 0 <= g0 <= g1 <= self.n_ctr:
+            raise ValueError("row range must satisfy 0 <= g0 <= g1 <= n_ctr, g0 % 32 == 0")
+        L = _lib.load()
+        dev = self.dev
+        st = dv.stream_handle(dev)
+        n = g1 - g0
+        lptr = self.ptr[g0:g1 + 1] - self.ptr[g0]
+        n_sl = (n + 31) // 32
+        wsb = int(L.tsqbx_sell_workspace_bytes(n))
+        sws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        sptr = torch.empty(n_sl + 1, dtype=torch.int64, device=dev)
+        tot = torch.zeros(2, dtype=torch.int64, device=dev)
+        _lib.check(L.tsqbx_sell_size(n, lptr.data_ptr(), sws.data_ptr(), wsb, sptr.data_ptr(),
+                                     tot[1:].data_ptr(), st), "tsqbx_sell_size")
+        sidx = torch.empty(max(int(tot[1].item()), 4), dtype=torch.int32, device=dev)
+        nptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        _lib.check(L.tsqbx_near_fill_rows(self.ctr.data_ptr(), self.rad.data_ptr(), self.n_ctr,
+                                          self.src.data_ptr(), self.n_src, self.ws.data_ptr(),
+                                          self.ws_bytes, self.ctr_order.data_ptr(), g0, g1,
+                                          nptr.data_ptr(), sptr.data_ptr(), sidx.data_ptr(),
+                                          tot.data_ptr(), st), "tsqbx_near_fill_rows")
+        return NearLists(n_ctr=n, n_src=self.n_src, n_pairs=int(lptr[-1].item()), ptr=nptr,
+                         csr_idx=None, src_perm=self.src_perm[:self.n_src], ctr_order=None,
+                         sell_ptr=sptr, sell_idx=sidx)

@@ -206,7 +206,9 @@ class _Prepared:
                rows: tuple[int, int] | None = None, out_offset: int = 0,
                user_order: bool = True) -> None:
         """One evaluation launch.  ``rows=(g0, g1)`` restricts it to a row range
-        (multi-GPU shard); ``user_order=False`` writes processing order."""
+        (a multi-GPU shard or one chunk of it).  The potential of processing-order
+        target t goes to ``out[tidx[t] - out_offset]`` (user order) or, with
+        ``user_order=False``, to ``out[t - out_offset]``."""
         L = _lib.load()
         flags = ((_lib.FLAG_VALIDATE if validate else 0) | (_lib.FLAG_GENERIC if generic else 0)
                  | (_lib.FLAG_REAL_WEIGHTS if self.real_w else 0)
@@ -214,13 +216,15 @@ class _Prepared:
         near = self.near
         g0, g1 = rows if rows is not None else (0, self.n_ctr)
         G = self.G
-        if self.tuni and (g0, g1) == (0, self.n_ctr):
+        if self.tuni:
+            # uniform runs: row g of the range owns targets tuni * (g0 + g) ...
             flags |= _lib.FLAG_UNIFORM_TARGETS | (self.tuni << 8)
-        elif self._auto_split and (g0, g1) != (0, self.n_ctr):
+        if self._auto_split and (g0, g1) != (0, self.n_ctr):
             # a row range (multi-GPU shard) fills fewer waves than the whole problem
             G = pick_split(self.near.mean_len, g1 - g0, self.n_tgt < 2 * self.n_ctr,
                            dv.sm_count(self.dev.index if self.dev.index is not None
-                                       else torch.cuda.current_device()))
+                                       else torch.cuda.current_device()),
+                           uniform=bool(self.tuni))
         sell = self.layout == "sell" and near.sell_ptr is not None
         if sell and g0 % 32:
             raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
@@ -234,7 +238,7 @@ class _Prepared:
             near.sell_ptr.data_ptr() + 8 * (g0 // 32) if sell else None,
             near.sell_idx.data_ptr() if sell else None, self.tgt.data_ptr(),
             dv.ptr(self.tn), self.tptr.data_ptr() + 8 * g0, self.n_tgt,
-            dv.ptr(self.tidx) if user_order else None, out_offset, flags, G,
+            dv.ptr(self.tidx) if user_order else None, out_offset, self.tuni * g0, flags, G,
             self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.err.data_ptr(),
             dv.stream_handle(self.dev)), "tsqbx_eval_packed")
 

@@ -44,16 +44,16 @@ def test_abi_queries_without_gpu():
 def test_abi_rejects_bad_arguments_without_launching():
     L = _lib.load()
     rc = L.tsqbx_eval_packed(7, 0, 0.0, 4, None, 0, 0, None, 0, None, None, None, None, None,
-                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT and "equation" in _lib.last_error()
     rc = L.tsqbx_eval_packed(1, 0, -1.0, 4, None, 0, 0, None, 0, None, None, None, None, None,
-                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT and "k > 0" in _lib.last_error()
     rc = L.tsqbx_eval_packed(0, 0, 0.0, 65, None, 0, 0, None, 0, None, None, None, None, None,
-                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT
     rc = L.tsqbx_eval_packed(0, 2, 0.0, 4, None, 0, 0, None, 0, None, None, None, None, None,
-                             None, None, 0, None, 0, 0, 8, None, 0, None, None, None)
+                             None, None, 0, None, 0, 0, 0, 8, None, 0, None, None, None)
     assert rc == _lib.ERR_ARGUMENT and "normals" in _lib.last_error()
 
 

@@ -1,4 +1,4 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): row sharding by pair
+"""Multi-rank host logic on CPU (gloo, world sizes 2 and 4): row sharding by pair
 count, padded all-gather layout, scatter back to user order.  The per-rank
 compute is the oracle here (the GPU kernel is covered by the gpu tests); the
 assembled result must be bit-identical to the single-process result."""
@@ -14,7 +14,8 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_1811_01110_b200 import configs
-from paper_1811_01110_b200.distributed import assemble_numpy, balanced_rows, make_plan
+from paper_1811_01110_b200.distributed import (assemble_numpy, balanced_rows, gather_chunks,
+                                                   make_layout)
 
 
 def test_balanced_rows_balances_pairs_and_aligns():
@@ -30,13 +31,21 @@ def test_balanced_rows_balances_pairs_and_aligns():
     assert b[0] == 0 and b[-1] == 10
 
 
-def test_plan_dest_covers_every_target_once():
-    row_len = np.array([3, 0, 5, 2, 7, 1] * 20)
-    tptr = np.concatenate([[0], np.cumsum(np.tile([2, 1, 0, 3, 1, 2], 20))])
-    tidx = np.random.default_rng(1).permutation(tptr[-1])
-    plan = make_plan(row_len, tptr, tidx, 3)
-    d = plan.dest[plan.dest < plan.n_tgt]
-    assert np.array_equal(np.sort(d), np.arange(plan.n_tgt))
+@pytest.mark.parametrize("world,chunks", [(1, 1), (2, 1), (3, 4), (8, 3)])
+def test_layout_dest_covers_every_target_once(world, chunks):
+    rng = np.random.default_rng(1)
+    tpc = np.tile([2, 1, 0, 3, 1, 2], 200)
+    row_len = rng.integers(0, 9, size=tpc.size)
+    tptr = np.concatenate([[0], np.cumsum(tpc)])
+    tidx = rng.permutation(tptr[-1])
+    L = make_layout(row_len * tpc, tptr, tidx, world, chunks)
+    d = L.dest[L.dest < L.n_tgt]
+    assert np.array_equal(np.sort(d), np.arange(L.n_tgt))
+    assert L.dest.size == world * L.send_len
+    assert np.all(L.chunk_rows[:, 1:-1] % 32 == 0) and np.all(L.row_bounds[1:-1] % 32 == 0)
+    assert np.array_equal(L.chunk_rows[:, 0], L.row_bounds[:-1])
+    assert np.array_equal(L.chunk_rows[:, -1], L.row_bounds[1:])
+    assert np.all(np.diff(L.chunk_tgts, axis=1) <= L.pad[None, :])
 
 
 def _free_port():
@@ -45,23 +54,44 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, chunks, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    case = configs.make_case("c2", "literal", n=512)
+    case = configs.make_case("c2", "literal", n=2048)
     ptr, idx = oracle.near_csr(case.centers, case.near_radii, case.sources)
-    plan = make_plan(np.diff(ptr), case.tgt_ptr, None, world)
-    g0, g1 = plan.rows(rank)
-    t0, t1 = plan.targets(rank)
-    sub = oracle.ts_batch("laplace", 0, 0.0, 8, case.sources, case.weights,
-                          case.centers[g0:g1], ptr[g0:g1 + 1] - ptr[g0], idx[ptr[g0]:ptr[g1]],
-                          case.targets[t0:t1], case.tgt_ptr[g0:g1 + 1] - case.tgt_ptr[g0])
-    send = torch.zeros(plan.shard, dtype=torch.complex128)
-    send[:t1 - t0] = torch.from_numpy(sub)
-    recv = torch.zeros(world * plan.shard, dtype=torch.complex128)
-    dist.all_gather_into_tensor(recv, send)
-    out = assemble_numpy(recv.numpy(), plan)
+    # a processing order that is not the identity (as the device Morton order)
+    order = np.random.default_rng(5).permutation(case.n_centers)
+    lens = np.diff(ptr)[order]
+    tl = np.diff(case.tgt_ptr)[order]
+    tptr_p = np.concatenate([[0], np.cumsum(tl)])
+    tidx = np.concatenate([np.arange(case.tgt_ptr[c], case.tgt_ptr[c + 1]) for c in order])
+    L = make_layout(lens * tl, tptr_p, tidx, world, chunks)
+    send = torch.zeros(L.send_len, dtype=torch.complex128)
+    recv = torch.zeros(world * L.send_len, dtype=torch.complex128)
+
+    def launch_chunk(c):
+        # this rank's chunk c, evaluated by the oracle (the GPU kernel stands here)
+        g0, g1 = int(L.chunk_rows[rank, c]), int(L.chunk_rows[rank, c + 1])
+        if g1 <= g0:
+            return
+        ctr = order[g0:g1]
+        sptr = np.concatenate([[0], np.cumsum(np.diff(ptr)[ctr])])
+        sidx = np.concatenate([idx[ptr[c_]:ptr[c_ + 1]] for c_ in ctr])
+        t0, t1 = int(L.chunk_tgts[rank, c]), int(L.chunk_tgts[rank, c + 1])
+        sub = oracle.ts_batch("laplace", 0, 0.0, 8, case.sources, case.weights,
+                              case.centers[ctr], sptr, sidx, case.targets[tidx[t0:t1]],
+                              tptr_p[g0:g1 + 1] - tptr_p[g0])
+        a = int(L.send_off[c])
+        send[a:a + (t1 - t0)] = torch.from_numpy(sub)
+
+    if world > 1:
+        gather_chunks(send, recv, L, launch_chunk=launch_chunk)
+    else:
+        for c in range(L.chunks):
+            launch_chunk(c)
+        recv = send
+    out = assemble_numpy(recv.numpy(), L)
     if rank == 0:
         full = oracle.ts_batch("laplace", 0, 0.0, 8, case.sources, case.weights, case.centers,
                                ptr, idx, case.targets, case.tgt_ptr)
@@ -70,11 +100,12 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_allgather_matches_single_process():
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (4, 4)])
+def test_multi_rank_chunked_allgather_matches_single_process(world, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, chunks, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
