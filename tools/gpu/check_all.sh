@@ -1,0 +1,6 @@
+set -x
+python -m pytest tests/test_gpu_distributed.py -x -q > gpurun_out/t_dist.log 2>&1; echo rc=$? >> gpurun_out/t_dist.log
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.log 2>&1; echo rc=$? >> gpurun_out/t_all.log
+python bench.py --steps 10 --warmup 3 --no-secondary > gpurun_out/b1.json 2> gpurun_out/b1.err; echo rc=$? >> gpurun_out/b1.err
+NCCL_DEBUG=WARN timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --force-dist --steps 10 --warmup 3 > gpurun_out/bd.json 2> gpurun_out/bd.err; echo rc=$? >> gpurun_out/bd.err
+timeout 600 python bench.py --impl reference --steps 5 --warmup 2 > gpurun_out/bref.json 2> gpurun_out/bref.err; echo rc=$? >> gpurun_out/bref.err
