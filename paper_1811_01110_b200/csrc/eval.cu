@@ -617,6 +617,7 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   a.log2G = __builtin_ctz((unsigned)G);
   a.validate = val ? 1 : 0;
   a.k = k;
+  a.sc = kSincCos;
   if (equation == TSQBX_EQ_HELMHOLTZ) {
     a.ttab_stride = fast ? p + 1 : 2 * (p + 1);
     const int64_t need = n_tgt * a.ttab_stride * (int64_t)sizeof(double);

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kSellBlock, VARIANT == 2 ? 2 : 1) helmholtz_de
       const double iR = rsqrt_fast(R2);
       const double invx = iR * invk;
       double hmr, hmi, hcr, hci;                       // h_{n-1}, h_n, starting at n = 1
-      hankel01(k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
+      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
       double nss = 0.0;
       if (VARIANT == 2) nss = fma(n4.z, dz, fma(n4.y, dy, n4.x * dx)) * iR;
       double cg[NT], pm[NT], pc[NT], dm[NT], dc[NT], ar_[NT], ai_[NT], br_[NT], bi_[NT];

@@ -2,6 +2,12 @@
 // SELL-32x4 thread-per-row kernel and the CSR group kernel.
 #include "eval_kernels.cuh"
 
+// 1: the SELL S kernel sums over orders by Clenshaw on the Hankel recurrence
+// (5 DP instructions per order); 0: forward complex Hankel recurrence (8)
+#ifndef TSQBX_HELM_CLENSHAW
+#define TSQBX_HELM_CLENSHAW 1
+#endif
+
 namespace tsqbx {
 
 // ---------------------------------------------------------------------------
@@ -51,7 +57,7 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
       double hr[P + 1], hi[P + 1];
       {
         double h1r, h1i;
-        hankel01(k2 * R2, x, invx, hr[0], hi[0], h1r, h1i);
+        hankel01(a.sc, k2 * R2, x, invx, hr[0], hi[0], h1r, h1i);
         if constexpr (P >= 1) {
           hr[1] = h1r;
           hi[1] = h1i;
@@ -117,6 +123,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
   // registers, fewer spills: C5 literal +9 %, dense +2 %); with two targets the
   // register copy is faster (C3 dense -1.5 % from shared memory)
   constexpr bool kCfShared = NT == 1;
+  constexpr bool kClenshaw = TSQBX_HELM_CLENSHAW != 0;
   extern __shared__ double cfs[];
   double cfr[kCfShared ? 1 : NT][kCfShared ? 1 : P + 1];
   auto cf = [&](int n, int q) -> double& {
@@ -161,7 +168,8 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
           for (int n = 0; n <= P; ++n) jn[n] = n == 0 && ok ? 1.0 : 0.0;
         }
 #pragma unroll
-        for (int n = 0; n <= P; ++n) CF(n, q) = (2.0 * n + 1.0) * jn[n] * c_leg.kappa[n];
+        for (int n = 0; n <= P; ++n)
+          CF(n, q) = kClenshaw ? c_leg.hsc[n] * jn[n] : (2.0 * n + 1.0) * jn[n] * c_leg.kappa[n];
       }
       ar[q] = ai[q] = 0.0;
     }
@@ -175,8 +183,53 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
       const double iR = rsqrt_fast(R2);
       const double invx = iR * invk;
       double hmr, hmi, hcr, hci;                 // h_{n-1}, h_n
-      hankel01(k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
+      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
       double cg[NT], pm[NT], pc[NT], sr[NT], si[NT];
+      if constexpr (kClenshaw) {
+        // sum_n a_n h_n, a_n = c_n P_n(cos g) real, by Clenshaw over the Hankel
+        // recurrence h_{n+1} = (2n+1) u h_n - h_{n-1} (u = 1/x, _core.pyx:192-193):
+        // y_n = a_n + (2n+1) u y_{n+1} - y_{n+2}, sum = h_0 (a_0 - y_2) + h_1 y_1.
+        // With g_n = (2n-1)!! y_n the middle coefficient is u itself:
+        // g_n = (2n-1)!! a_n + u g_{n+1} - g_{n+2} / ((2n+1)(2n+3)), y_1 = g_1,
+        // y_2 = g_2 / 3.  The scaled a'_n = (2n-1)!! a_n come from the Legendre
+        // recurrence (stored: Clenshaw runs downward), so each order costs 5 DP
+        // instructions (Legendre 2, a'_n 1, Clenshaw 2) against 8 for the
+        // forward complex Hankel recurrence -- and the h_n are never formed.
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          cg[q] = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
+          double ap[P + 1];
+          if constexpr (P >= 1) {
+            double um = 1.0, uc = cg[q];
+            ap[1] = CF(1, q) * uc;
+#pragma unroll
+            for (int n = 1; n < P; ++n) {
+              const double un = fma(c_leg.alpha[n] * cg[q], uc, -um);
+              um = uc;
+              uc = un;
+              ap[n + 1] = CF(n + 1, q) * un;
+            }
+          }
+          double g1 = 0.0, g2 = 0.0;            // g_{n+1}, g_{n+2}
+          if constexpr (P >= 1) {
+            g1 = ap[P];                          // g_P
+            if constexpr (P >= 2) {
+              g2 = g1;
+              g1 = fma(invx, g2, ap[P - 1]);     // g_{P-1}
+            }
+#pragma unroll
+            for (int n = P - 2; n >= 1; --n) {
+              const double g = fma(invx, g1, fma(-c_leg.gam[n], g2, ap[n]));
+              g2 = g1;
+              g1 = g;
+            }
+          }
+          // sum = h_0 (a_0 - g_2 / 3) + h_1 g_1
+          const double t0 = P >= 2 ? fma(-1.0 / 3.0, g2, CF(0, q)) : CF(0, q);
+          sr[q] = fma(hcr, g1, hmr * t0);
+          si[q] = fma(hci, g1, hmi * t0);
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         cg[q] = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;
@@ -210,6 +263,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
           si[q] = fma(c, hni, si[q]);
         }
       }
+      }   // forward recurrence
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         ar[q] = fma(q4.w, sr[q], fma(-wim, si[q], ar[q]));

@@ -37,6 +37,7 @@ struct EvalParams {
   int tuni;                          // k > 0: row g owns targets [k g, k g + k) (no tptr load)
   const unsigned* __restrict__ imag_flag;   // device: pack_kernel saw Im w != 0
   double k;
+  SincCosCoeffs sc;                  // sin/cos series (kSincCos), constant-bank operands
 };
 
 int64_t packed_doubles(int64_t n, int with_normals);
