@@ -58,6 +58,15 @@ extern "C" {
 /* eval: every row g owns targets [k g, k g + k) (tgt_ptr[g] == k g), k = (flags >> 8) & 0xff;
  * the SELL kernels then address a row's targets without loading tgt_ptr */
 #define TSQBX_FLAG_UNIFORM_TARGETS 32u
+/* Helmholtz: the caller guarantees k |s - c| <= pi/4 (NARROW) or <= pi/2 (WIDE)
+ * for every near source of every row (e.g. k x the largest near radius):
+ * the kernels then take one sin/cos series for every lane without a warp
+ * vote.  Without either flag each warp picks the series its lanes need. */
+#define TSQBX_FLAG_KR_NARROW 64u
+#define TSQBX_FLAG_KR_WIDE 128u
+/* a performance hint: the near lists are long (mean >~ 48 entries), pick the
+ * kernel builds tuned for long rows (never changes results) */
+#define TSQBX_FLAG_LONG_ROWS (1u << 16)
 
 #define TSQBX_MAX_ORDER 64
 

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kSellBlock, VARIANT == 2 ? 2 : 1) helmholtz_de
       // j_0..j_{P+1}(k r) -> term coefficients (j_n(0) = delta_n0, j'_1(0) = 1/3)
       double jn[P + 2];
       if (ok && rr > 0.0) {
-        miller_j_reg<P + 2>(k * rr, jn);
+        sph_j_reg<P + 2>(k * rr, jn);
       } else {
 #pragma unroll
         for (int n = 0; n <= P + 1; ++n) jn[n] = (n == 0 && ok) ? 1.0 : 0.0;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kSellBlock, VARIANT == 2 ? 2 : 1) helmholtz_de
       const double iR = rsqrt_fast(R2);
       const double invx = iR * invk;
       double hmr, hmi, hcr, hci;                       // h_{n-1}, h_n, starting at n = 1
-      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
+      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci, a.series);
       double nss = 0.0;
       if (VARIANT == 2) nss = fma(n4.z, dz, fma(n4.y, dy, n4.x * dx)) * iR;
       double cg[NT], pm[NT], pc[NT], dm[NT], dc[NT], ar_[NT], ai_[NT], br_[NT], bi_[NT];

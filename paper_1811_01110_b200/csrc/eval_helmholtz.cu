@@ -115,14 +115,18 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
 
 // UNI = NT: uniform target runs (row g owns targets [NT g, NT g + NT)), one
 // pass and no tgt_ptr loads (TSQBX_FLAG_UNIFORM_TARGETS)
-template <int P, int NT, bool VAL, int UNI>
-__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
+// CFR (one target per center only): 1 = the target coefficients in registers
+// with 2 CTAs per SM instead of shared memory with 3 -- long rows (dense
+// presets: C5 dense -2 %), where the extra warps of the 3-CTA build only help
+// short rows hide their per-row latency (C5 literal +14 %)
+template <int P, int NT, bool VAL, int UNI, int CFR = 0>
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? (CFR ? 2 : TSQBX_HELM_MINB1) : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
   // per-thread target coefficients c_n = (2n+1) j_n(k r) kappa_n, in registers
   // (a shared-memory copy measured slower)
   // one target per center: the coefficients live in shared memory (fewer
   // registers, fewer spills: C5 literal +9 %, dense +2 %); with two targets the
   // register copy is faster (C3 dense -1.5 % from shared memory)
-  constexpr bool kCfShared = NT == 1;
+  constexpr bool kCfShared = NT == 1 && !CFR;
   constexpr bool kClenshaw = TSQBX_HELM_CLENSHAW != 0;
   extern __shared__ double cfs[];
   double cfr[kCfShared ? 1 : NT][kCfShared ? 1 : P + 1];
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
         double jn[P + 1];
         const double rr = r2[q] * ir;                 // |t - c|
         if (ok && rr > 0.0) {
-          miller_j_reg<P + 1>(k * rr, jn);
+          sph_j_reg<P + 1>(k * rr, jn);
         } else {
 #pragma unroll
           for (int n = 0; n <= P; ++n) jn[n] = n == 0 && ok ? 1.0 : 0.0;
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_HELM_MINB1 : TSQBX
       const double iR = rsqrt_fast(R2);
       const double invx = iR * invk;
       double hmr, hmi, hcr, hci;                 // h_{n-1}, h_n
-      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci);
+      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci, a.series);
       double cg[NT], pm[NT], pc[NT], sr[NT], si[NT];
       if constexpr (kClenshaw) {
         // sum_n a_n h_n, a_n = c_n P_n(cos g) real, by Clenshaw over the Hankel
@@ -301,9 +305,20 @@ struct HelmholtzLaunch {
   static void one(bool sell, const EvalParams& a, int64_t n_ctr, cudaStream_t st) {
     if (sell)
     {
-      const int smem = NT == 1 ? (P + 1) * kSellBlock * (int)sizeof(double) : 0;
-      (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT> : helmholtz_sell_kernel<P, NT, VAL, 0>)
-          <<<(int)((n_ctr + kSellBlock - 1) / kSellBlock), kSellBlock, smem, st>>>(a);
+      const int grid = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
+      bool done = false;
+      if constexpr (NT == 1) {
+        if (a.long_rows) {
+          (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT, 1>
+                        : helmholtz_sell_kernel<P, NT, VAL, 0, 1>)<<<grid, kSellBlock, 0, st>>>(a);
+          done = true;
+        }
+      }
+      if (!done) {
+        const int smem = NT == 1 ? (P + 1) * kSellBlock * (int)sizeof(double) : 0;
+        (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT>
+                      : helmholtz_sell_kernel<P, NT, VAL, 0>)<<<grid, kSellBlock, smem, st>>>(a);
+      }
     }
     else
       helmholtz_s_kernel<P, NT, VAL><<<(int)((n_ctr * a.G + 255) / 256), 256, 0, st>>>(a);

@@ -38,6 +38,8 @@ struct EvalParams {
   const unsigned* __restrict__ imag_flag;   // device: pack_kernel saw Im w != 0
   double k;
   SincCosCoeffs sc;                  // sin/cos series (kSincCos), constant-bank operands
+  int series;                        // 0: per-warp vote; 1: narrow only; 2: wide (library past pi/2)
+  int long_rows;                     // TSQBX_FLAG_LONG_ROWS: kernels tuned for long near lists
 };
 
 int64_t packed_doubles(int64_t n, int with_normals);

@@ -340,7 +340,10 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
     const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
   constexpr bool FILL = MODE == 1;
-  __shared__ double4 tile[4][kTile];
+  // staged candidates as fp32 offsets from the warp's reference point (see
+  // run_cells) plus their sorted index; the exact fp64 test reads sxyz only for
+  // the rare candidates inside the fp32 error band
+  __shared__ float4 tile[4][kTile];
   __shared__ int32_t tid_[4][kTile];
   __shared__ int32_t cell_st[4][64], cell_en[4][64];   // compacted union cells per warp
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -375,7 +378,19 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
   int64_t ub = 0;                      // MODE 2: candidates this row will test
   // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
   // c % 32, slot c / 32) through the tile; lanes with `mine` test them all.
-  auto run_cells = [&](int ncell, int stA, int enA, int stB, int enB, bool mine) {
+  // o: the reference point (a center of this warp); A: a bound on |p - o|
+  // (max norm) of every staged source and every testing lane's center.
+  auto run_cells = [&](int ncell, int stA, int enA, int stB, int enB, bool mine, double ox,
+                       double oy, double oz, double A) {
+    // fp32 prefilter: with every coordinate offset from o (|.| <= A) rounded
+    // to fp32, |d2_f32 - d2| <= ~100 u A^2 (u = 2^-24); candidates with
+    // |d2_f32 - rad^2| <= 2^-16 A^2 take the exact fp64 test (member()), the
+    // rest are decided in fp32 -- membership stays bit-identical to the
+    // oracle, at ~1/3 of the FP64-pipe cost per candidate
+    const float tau = (float)(A * A * (1.0 / 65536.0));
+    const float r2f = (float)rad2;
+    const float rlo = r2f - tau, rhi = r2f + tau;
+    const float cfx = (float)(cx - ox), cfy = (float)(cy - oy), cfz = (float)(cz - oz);
     // exclusive prefix of the cell sizes (cell c in lane c % 32, slot c / 32)
     // so that a tile of candidates spanning many small cells is staged with
     // all its loads in flight at once (one latency per tile, not per cell)
@@ -414,7 +429,9 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
             else hi_c = mid - 1;
           }
           const int j = cell_st[wib][lo_c] + (t - cell_en[wib][lo_c]);
-          tile[wib][q] = sxyz[j];
+          const double4 sj = sxyz[j];
+          tile[wib][q] = make_float4((float)(sj.x - ox), (float)(sj.y - oy), (float)(sj.z - oz),
+                                     0.0f);
           tid_[wib][q] = j;
         }
       }
@@ -426,8 +443,16 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
           const int m = min(32, fill - t0);
           unsigned bits = 0u;
 #pragma unroll 8
-          for (int u = 0; u < 32; ++u)
-            if (u < m && member(tile[wib][t0 + u], cx, cy, cz, rad2)) bits |= 1u << u;
+          for (int u = 0; u < 32; ++u) {
+            if (u < m) {
+              const float4 v = tile[wib][t0 + u];
+              const float dx = v.x - cfx, dy = v.y - cfy, dz = v.z - cfz;
+              const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+              bool in = d2 <= rlo;
+              if (!in && d2 <= rhi) in = member(sxyz[tid_[wib][t0 + u]], cx, cy, cz, rad2);
+              if (in) bits |= 1u << u;
+            }
+          }
           if (!FILL) {
             k += __popc(bits);
           } else if (!row) {
@@ -521,7 +546,14 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
       for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
       ub = tot;
     } else if (n_ne > 0) {
-      run_cells(n_ne, stA, enA, stB, enB, valid);
+      // reference point: the first valid lane's center; every staged source
+      // and every lane center lies in the union box of ex x ey x ez cells
+      const int l0 = __ffs(__ballot_sync(0xffffffffu, valid)) - 1;
+      const double ox = __shfl_sync(0xffffffffu, cx, l0), oy = __shfl_sync(0xffffffffu, cy, l0),
+                   oz = __shfl_sync(0xffffffffu, cz, l0);
+      const double cs = prm[3] * (double)(1ull << (kSubBits + (lv_hi < 0 ? 0 : lv_hi)));
+      const double A = (double)(max(ex, max(ey, ez)) + 1) * cs;
+      run_cells(n_ne, stA, enA, stB, enB, valid, ox, oy, oz, A);
     }
   } else {
     // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
@@ -545,7 +577,12 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
         for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
         if (valid && ckey == cell) ub = tot;
       } else {
-        run_cells(27, st, en, 0, 0, valid && ckey == cell);
+        // reference point: the head lane's center; sources in the 3 x 3 x 3
+        // cells around its cell, testing lanes' centers in that cell
+        const double ox = __shfl_sync(0xffffffffu, cx, a), oy = __shfl_sync(0xffffffffu, cy, a),
+                     oz = __shfl_sync(0xffffffffu, cz, a);
+        const double A = 4.0 * prm[3] * (double)(1ull << (kSubBits + bl));
+        run_cells(27, st, en, 0, 0, valid && ckey == cell, ox, oy, oz, A);
       }
     }
   }

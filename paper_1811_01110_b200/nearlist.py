@@ -46,6 +46,7 @@ class NearLists:
     ctr_order: torch.Tensor | None = None
     sell_ptr: torch.Tensor | None = None
     sell_idx: torch.Tensor | None = None
+    max_radius: float | None = None      # every entry has |s - c| <= max_radius (None: unknown)
 
     @property
     def dev(self) -> torch.device:
@@ -233,7 +234,8 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
     return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr,
                      csr_idx=None if idx is None else idx[:n_pairs],
                      src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],
-                     sell_ptr=sptr, sell_idx=sidx)
+                     sell_ptr=sptr, sell_idx=sidx,
+                     max_radius=float(rad.max().item()) if n_ctr else 0.0)
 
 
 class NearRowBuilder:
@@ -273,6 +275,7 @@ class NearRowBuilder:
                                       self.ctr_order.data_ptr(), self.ptr.data_ptr(), None,
                                       self.totals.data_ptr(), st), "tsqbx_near_count")
         self.n_pairs = int(self.totals[0].item())
+        self.max_radius = float(self.rad.max().item()) if self.n_ctr else 0.0
 
     @property
     def row_lengths(self) -> torch.Tensor:
@@ -308,4 +311,4 @@ class NearRowBuilder:
                                           tot.data_ptr(), st), "tsqbx_near_fill_rows")
         return NearLists(n_ctr=n, n_src=self.n_src, n_pairs=int(lptr[-1].item()), ptr=nptr,
                          csr_idx=None, src_perm=self.src_perm[:self.n_src], ctr_order=None,
-                         sell_ptr=sptr, sell_idx=sidx)
+                         sell_ptr=sptr, sell_idx=sidx, max_radius=self.max_radius)

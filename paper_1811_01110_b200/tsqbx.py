@@ -174,6 +174,14 @@ class _Prepared:
         self.tuni = 0         # k > 0: every row owns k consecutive targets (set_uniform_targets)
         self._auto_split = (not group_lanes and self.layout == "sell" and spec.is_laplace
                             and self.variant == 0 and "GIGAQBX_SPLIT" not in os.environ)
+        # Helmholtz: every near source lies within the largest near radius, so
+        # k R is bounded and the kernels can take one sin/cos series without a
+        # per-warp vote (the bound is exact: the lists test |s-c|^2 <= rad^2)
+        self.kr_flag = 0
+        if not spec.is_laplace and near.max_radius is not None:
+            kr = self.k * near.max_radius * (1.0 + 1e-12)
+            self.kr_flag = (_lib.FLAG_KR_NARROW if kr <= math.pi / 4 else
+                            _lib.FLAG_KR_WIDE if kr <= math.pi / 2 else 0)
 
     def set_uniform_targets(self, known: bool = False) -> None:
         """Let the SELL kernels address row g's targets as [k g, k g + k) instead of
@@ -212,7 +220,8 @@ class _Prepared:
         L = _lib.load()
         flags = ((_lib.FLAG_VALIDATE if validate else 0) | (_lib.FLAG_GENERIC if generic else 0)
                  | (_lib.FLAG_REAL_WEIGHTS if self.real_w else 0)
-                 | (_lib.FLAG_ONE_TARGET if self.one_target else 0))
+                 | (_lib.FLAG_ONE_TARGET if self.one_target else 0) | self.kr_flag
+                 | (_lib.FLAG_LONG_ROWS if self.near.mean_len >= 48 else 0))
         near = self.near
         g0, g1 = rows if rows is not None else (0, self.n_ctr)
         G = self.G
