@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 8
+#define TSQBX_ABI_VERSION 9
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -203,6 +203,14 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                     const int32_t* ctr_order, int64_t* near_ptr, int32_t* near_idx,
                     const int64_t* sell_ptr, int32_t* sell_idx, int64_t* totals,
                     void* stream);
+/* After a SELL-mode tsqbx_near_count (same workspace, no call in between but
+ * tsqbx_sell_size): count every row exactly, reusing its sorts and cell hash,
+ * into near_ptr (n_ctr + 1) and totals[0] = n_pairs -- the exact-size route
+ * when the bound-sized SELL buffer would be too large.  No synchronisation. */
+int tsqbx_near_recount(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                       int64_t n_src, void* workspace, int64_t ws_bytes,
+                       const int32_t* ctr_order, int64_t* near_ptr, int64_t* totals,
+                       void* stream);
 /* Rows g0..g1-1 of the processing order only (a rank's shard),
  * SELL mode: after tsqbx_near_count over ALL centers (CSR mode: exact row
  * lengths), the caller sizes the shard's slices from near_ptr[g0..g1] (e.g.

@@ -44,7 +44,10 @@ constexpr int kLevels = 4;
 // stays in L2 and the extra inserts and lookups cost more than the candidate
 // tests they save (C5 literal, 8.4 M sources: 10.8 ms one level, 12.3 ms four;
 // C4 literal, 1 M sources: 1.87 ms one level, 1.53 ms four).
-constexpr int64_t kMultiLevelMaxSources = 1 << 20;
+#ifndef TSQBX_MULTILEVEL_MAX_SRC
+#define TSQBX_MULTILEVEL_MAX_SRC (1 << 20)
+#endif
+constexpr int64_t kMultiLevelMaxSources = TSQBX_MULTILEVEL_MAX_SRC;
 constexpr int kFineOffset = 1 << (kSubBits + kLevels - 1);  // coarse coordinate >= 1 at every level
 
 struct NearLayout {
@@ -326,9 +329,16 @@ __device__ __forceinline__ bool member(const double4 s, double cx, double cy, do
 // 128-candidate tiles and <= 64 registers (8 CTAs of 128 threads per SM):
 // measured equal on dense lists, 9 % faster on the literal preset
 constexpr int kTile = 128;
+constexpr int kMaxCells = 128;   // cells one union pass stages (non-empty ones)
+// fill: members of the busiest lane in a 32-candidate group from which the
+// append walks all 32 candidates instead of each lane's own members
+#ifndef TSQBX_WALK_ABOVE
+#define TSQBX_WALK_ABOVE 20
+#endif
+constexpr unsigned kWalkAbove = TSQBX_WALK_ABOVE;
 
-// MODE 0: count members per row; 1: fill (SELL column and/or CSR row, plus
-// the row length when `cnt` is given); 2: bound -- no distance tests, the
+// MODE 0: count members per row; 1: fill the SELL column (plus the row length
+// when `cnt` is given); 3: fill the CSR row; 2: bound -- no distance tests, the
 // slice width (32 x the largest candidate count of its rows, a multiple of 4)
 // into `cnt[slice]`, so the fill can write before the exact lengths are known.
 template <int MODE>
@@ -339,13 +349,15 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
     int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
     const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
-  constexpr bool FILL = MODE == 1;
+  constexpr bool FILL = MODE == 1 || MODE == 3;
   // staged candidates as fp32 offsets from the warp's reference point (see
   // run_cells) plus their sorted index; the exact fp64 test reads sxyz only for
   // the rare candidates inside the fp32 error band
-  __shared__ float4 tile[4][kTile];
+  // candidate pairs for the packed-fp32 (FFMA2) test: pair p of the tile is
+  // tab[p] = {x0, x1, y0, y1}, tcd[p] = {z0, z1, w0, w1}
+  __shared__ float4 tab[4][kTile / 2], tcd[4][kTile / 2];
   __shared__ int32_t tid_[4][kTile];
-  __shared__ int32_t cell_st[4][64], cell_en[4][64];   // compacted union cells per warp
+  __shared__ int32_t cell_st[4][kMaxCells], cell_en[4][kMaxCells];   // a warp's cell list
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = g < n_ctr;
@@ -369,52 +381,53 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     ccz = f[2] >> (kSubBits + lv);
     ckey = morton3(ccx, ccy, ccz) | level_tag(lv);
   }
-  int32_t* row = (FILL && valid && nidx) ? nidx + nptr[g] : nullptr;
-  // SELL-32x4 column of this row as int4 blocks: block b at sblk[32 b]
-  int4* sblk = (FILL && valid && sidx) ? reinterpret_cast<int4*>(sidx + sptr[g >> 5]) + (g & 31)
-                                       : nullptr;
+  // MODE 3: CSR row; MODE 1: SELL-32x4 column, entry k at dst[128 (k / 4) + k % 4]
+  int32_t* dst = (MODE == 3 && valid) ? nidx + nptr[g]
+                 : (MODE == 1 && valid) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
   int k = 0;
-  int4 pend = make_int4(0, 0, 0, 0);   // fill, SELL only: the row's current block
   int64_t ub = 0;                      // MODE 2: candidates this row will test
-  // Stage the sources of a list of up to 64 cells (cell c's range sits in lane
-  // c % 32, slot c / 32) through the tile; lanes with `mine` test them all.
-  // o: the reference point (a center of this warp); A: a bound on |p - o|
-  // (max norm) of every staged source and every testing lane's center.
-  auto run_cells = [&](int ncell, int stA, int enA, int stB, int enB, bool mine, double ox,
-                       double oy, double oz, double A) {
-    // fp32 prefilter: with every coordinate offset from o (|.| <= A) rounded
-    // to fp32, |d2_f32 - d2| <= ~100 u A^2 (u = 2^-24); candidates with
-    // |d2_f32 - rad^2| <= 2^-16 A^2 take the exact fp64 test (member()), the
-    // rest are decided in fp32 -- membership stays bit-identical to the
-    // oracle, at ~1/3 of the FP64-pipe cost per candidate
-    const float tau = (float)(A * A * (1.0 / 65536.0));
-    const float r2f = (float)rad2;
-    const float rlo = r2f - tau, rhi = r2f + tau;
-    const float cfx = (float)(cx - ox), cfy = (float)(cy - oy), cfz = (float)(cz - oz);
-    // exclusive prefix of the cell sizes (cell c in lane c % 32, slot c / 32)
-    // so that a tile of candidates spanning many small cells is staged with
-    // all its loads in flight at once (one latency per tile, not per cell)
-    const int szA = lane < ncell ? enA - stA : 0;
-    const int szB = lane + 32 < ncell ? enB - stB : 0;
-    int incA = szA, incB = szB;
+  // Stage the sources of a list of up to kMaxCells cells (ranges [st, en) in
+  // cell_st / cell_en of this warp, written by the caller) through the tile;
+  // lanes with `mine` test them all.  o: the reference point (a center of this
+  // warp); A: a bound on |p - o| (max norm) of every staged source and every
+  // testing lane's center.
+  auto run_cells = [&](int ncell, bool mine, double ox, double oy, double oz, double A) {
+    // fp32 prefilter in dot-product form: with s' = s - o, c' = c - o (every
+    // coordinate |.| <= A) a candidate is a member iff
+    //   f = s'.c' - |s'|^2 / 2  >=  K = (|c'|^2 - rad^2) / 2,
+    // i.e. three FFMAs per (candidate, lane) against a staged (s', -|s'|^2/2).
+    // Rounding s', c', w' and K to fp32 and the fp32 FMAs move f - K by at
+    // most ~40 u A^2 (u = 2^-24); candidates with |f - K| <= 2^-14 A^2 (> 10x
+    // that) take the exact fp64 test (member()) after the group, the rest are
+    // decided in fp32 -- membership stays bit-identical to the oracle
+    const float tau = (float)(A * A * (1.0 / 16384.0));
+    const double cdx = cx - ox, cdy = cy - oy, cdz = cz - oz;
+    const float K = (float)(0.5 * (cdx * cdx + cdy * cdy + cdz * cdz - rad2));
+    const float Khi = K + tau, Klo = K - tau;
+    const float cfx = (float)cdx, cfy = (float)cdy, cfz = (float)cdz;
+    // exclusive prefix of the cell sizes (cell c in lane c % 32, slot c / 32),
+    // kept in cell_en, so that a tile of candidates spanning many small cells
+    // is staged with all its loads in flight at once (one latency per tile)
+    int total = 0;
+    int pre[kMaxCells / 32];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, incA, off);
-      const int b = __shfl_up_sync(0xffffffffu, incB, off);
-      if (lane >= off) {
-        incA += a;
-        incB += b;
+    for (int q = 0; q < kMaxCells / 32; ++q) {
+      const int c = lane + 32 * q;
+      const int sz = c < ncell ? cell_en[wib][c] - cell_st[wib][c] : 0;
+      int inc = sz;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += a;
       }
+      pre[q] = total + inc - sz;
+      total += __shfl_sync(0xffffffffu, inc, 31);
     }
-    const int totA = __shfl_sync(0xffffffffu, incA, 31);
-    const int total = totA + __shfl_sync(0xffffffffu, incB, 31);
     __syncwarp();
-    cell_en[wib][lane] = incA - szA;             // cell_en now holds the prefix
-    cell_en[wib][lane + 32] = totA + incB - szB;
-    cell_st[wib][lane] = stA;
-    cell_st[wib][lane + 32] = stB;
+#pragma unroll
+    for (int q = 0; q < kMaxCells / 32; ++q) cell_en[wib][lane + 32 * q] = pre[q];
     __syncwarp();
-    const int nc = min(ncell, 64);
+    const int nc = min(ncell, kMaxCells);
     for (int base = 0; base < total; base += kTile) {
       const int fill = min(kTile, total - base);
 #pragma unroll
@@ -430,8 +443,13 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
           }
           const int j = cell_st[wib][lo_c] + (t - cell_en[wib][lo_c]);
           const double4 sj = sxyz[j];
-          tile[wib][q] = make_float4((float)(sj.x - ox), (float)(sj.y - oy), (float)(sj.z - oz),
-                                     0.0f);
+          const float x = (float)(sj.x - ox), y = (float)(sj.y - oy), z = (float)(sj.z - oz);
+          float* pa = reinterpret_cast<float*>(&tab[wib][q >> 1]) + (q & 1);
+          float* pc = reinterpret_cast<float*>(&tcd[wib][q >> 1]) + (q & 1);
+          pa[0] = x;
+          pa[2] = y;
+          pc[0] = z;
+          pc[2] = -0.5f * fmaf(z, z, fmaf(y, y, x * x));
           tid_[wib][q] = j;
         }
       }
@@ -441,43 +459,62 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
         // this lane's members (no per-candidate divergent work in the fill)
         for (int t0 = 0; t0 < fill; t0 += 32) {
           const int m = min(32, fill - t0);
-          unsigned bits = 0u;
-#pragma unroll 8
-          for (int u = 0; u < 32; ++u) {
-            if (u < m) {
-              const float4 v = tile[wib][t0 + u];
-              const float dx = v.x - cfx, dy = v.y - cfy, dz = v.z - cfz;
-              const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              bool in = d2 <= rlo;
-              if (!in && d2 <= rhi) in = member(sxyz[tid_[wib][t0 + u]], cx, cy, cz, rad2);
-              if (in) bits |= 1u << u;
-            }
+          // candidate u lands in bit 31 - u: each test shifts the sign bit of
+          // f - K -/+ tau into a mask with one funnel shift (SHF); candidates
+          // go in pairs through packed fp32 (FFMA2 / FADD2), so a pair costs
+          // 2 LDS.128 + 3 FFMA2 + 2 FADD2 + 4 SHF
+          unsigned below_hi = 0u, below_lo = 0u;
+          const float2 cx2 = make_float2(cfx, cfx), cy2 = make_float2(cfy, cfy),
+                       cz2 = make_float2(cfz, cfz);
+          const float2 nkhi = make_float2(-Khi, -Khi), nklo = make_float2(-Klo, -Klo);
+#pragma unroll 4
+          for (int u = 0; u < 32; u += 2) {
+            const float4 a = tab[wib][(t0 + u) >> 1], c = tcd[wib][(t0 + u) >> 1];
+            const float2 f = __ffma2_rn(make_float2(a.x, a.y), cx2,
+                                        __ffma2_rn(make_float2(a.z, a.w), cy2,
+                                                   __ffma2_rn(make_float2(c.x, c.y), cz2,
+                                                              make_float2(c.z, c.w))));
+            const float2 gh = __fadd2_rn(f, nkhi), gl = __fadd2_rn(f, nklo);
+            below_hi = __funnelshift_l(__float_as_uint(gh.x), below_hi, 1);
+            below_hi = __funnelshift_l(__float_as_uint(gh.y), below_hi, 1);
+            below_lo = __funnelshift_l(__float_as_uint(gl.x), below_lo, 1);
+            below_lo = __funnelshift_l(__float_as_uint(gl.y), below_lo, 1);
+          }
+          // slots past `m` hold stale candidates (low bits): masked, not branched on
+          const unsigned live = m == 32 ? ~0u : ~((1u << (32 - m)) - 1u);
+          unsigned bits = ~below_hi & live;                 // surely inside
+          unsigned band = below_hi & ~below_lo & live;      // within tau of the sphere
+          while (band) {                     // rare: the exact fp64 test
+            const int u = __clz(band);
+            band &= ~(0x80000000u >> u);
+            if (member(sxyz[tid_[wib][t0 + u]], cx, cy, cz, rad2)) bits |= 0x80000000u >> u;
           }
           if (!FILL) {
             k += __popc(bits);
-          } else if (!row) {
-            // SELL only: collect 4 members, then one 16-byte store of the block
-            while (bits) {
-              const int u = __ffs(bits) - 1;
-              bits &= bits - 1;
-              const int j = tid_[wib][t0 + u];
-              const int e = k & 3;
-              pend.x = e == 0 ? j : pend.x;
-              pend.y = e == 1 ? j : pend.y;
-              pend.z = e == 2 ? j : pend.z;
-              pend.w = j;
-              if (e == 3 && sblk) sblk[32 * (k >> 2)] = pend;
-              ++k;
-            }
           } else {
-            int32_t* scol = reinterpret_cast<int32_t*>(sblk);
-            while (bits) {
-              const int u = __ffs(bits) - 1;
-              bits &= bits - 1;
-              const int j = tid_[wib][t0 + u];
-              if (row) row[k] = j;
-              if (scol) scol[128 * (k >> 2) + (k & 3)] = j;   // entry k of this row's column
+            // append this lane's members to its row in candidate order.  A group
+            // of 32 Morton-consecutive candidates is spatially compact, so a
+            // lane whose ball covers it takes most of it while others take none:
+            // with many members per lane a uniform walk over the candidates
+            // (every lane stores its own) beats a per-lane loop that runs as
+            // long as the busiest lane
+            auto put = [&](int j) {
+              dst[MODE == 3 ? k : ((k >> 2) << 7) | (k & 3)] = j;
               ++k;
+            };
+            // (only the lanes testing this list are active here: per-cell mode)
+            if (__reduce_max_sync(__activemask(), (unsigned)__popc(bits)) >= kWalkAbove) {
+#pragma unroll 4
+              for (int u = 0; u < 32; ++u) {
+                const int j = tid_[wib][t0 + u];
+                if ((int)(bits << u) < 0) put(j);
+              }
+            } else {
+              while (bits) {
+                const int u = __clz(bits);      // candidate order: bit 31 - u
+                bits &= ~(0x80000000u >> u);
+                put(tid_[wib][t0 + u]);
+              }
             }
           }
         }
@@ -490,72 +527,97 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     st = en = 0;
     if (!hash_find(hkey, hst, hen, cap, morton3(x, y, z) | level_tag(level), st, en)) en = st;
   };
-  // Union mode: when the warp's centers sit in a small block of cells, every
-  // lane scans the union of their neighbourhoods at once (all lanes busy);
-  // candidates outside a lane's own 27 cells simply fail the distance test.
-  unsigned long long lo[3] = {valid ? ccx : ~0ull, valid ? ccy : ~0ull, valid ? ccz : ~0ull};
-  unsigned long long hi[3] = {valid ? ccx : 0ull, valid ? ccy : 0ull, valid ? ccz : 0ull};
+  // Union mode: every lane scans every cell that meets the warp's region
+  // [bbox - Rmax, bbox + Rmax] (bbox of its 32 centers, Rmax their largest
+  // radius) at the finest cell level where those cells number <= kMaxCells;
+  // candidates outside a lane's own ball simply fail the distance test.  Any
+  // level works here (not only cells >= r), so literal radii (a few sources
+  // per center, cells smaller than the warp's span) use a coarser level
+  // instead of falling back to the per-cell mode below.
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double blo[3] = {valid ? cx : inf, valid ? cy : inf, valid ? cz : inf};
+  double bhi[3] = {valid ? cx : -inf, valid ? cy : -inf, valid ? cz : -inf};
+  double rmx = valid ? sqrt(rad2) : 0.0;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      lo[d] = min(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], off));
-      hi[d] = max(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], off));
+      blo[d] = fmin(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], off));
+      bhi[d] = fmax(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], off));
+    }
+    rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, off));
+  }
+  const bool any_valid = __any_sync(0xffffffffu, valid);
+  // slack: the rounded membership test may accept a source a few ulps outside
+  // the exact ball; IEEE subtraction/division are monotone, so every source
+  // inside the slackened box maps into the box's corner cells
+  const double rb = rmx * (1.0 + 1e-9) + 1e-300;
+  int lw = -1;                          // union level
+  unsigned long long clo[3] = {0, 0, 0}, chi[3] = {0, 0, 0};
+  if (any_valid) {
+    const double plo[3] = {blo[0] - rb, blo[1] - rb, blo[2] - rb};
+    const double phi[3] = {bhi[0] + rb, bhi[1] + rb, bhi[2] + rb};
+    const double prm_l[4] = {prm[0], prm[1], prm[2], prm[3]};
+    unsigned long long flo[3], fhi[3];
+    fine_coords(plo, prm_l, flo);
+    fine_coords(phi, prm_l, fhi);
+    const int top = (int)prm[4];
+    for (int L = 0; L <= top; ++L) {
+      const int sh = kSubBits + L;
+      const unsigned long long n = ((fhi[0] >> sh) - (flo[0] >> sh) + 1) *
+                                   ((fhi[1] >> sh) - (flo[1] >> sh) + 1) *
+                                   ((fhi[2] >> sh) - (flo[2] >> sh) + 1);
+      if (n <= (unsigned long long)kMaxCells) {
+        lw = L;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          clo[d] = flo[d] >> sh;
+          chi[d] = fhi[d] >> sh;
+        }
+        break;
+      }
     }
   }
-  const unsigned long long ex = hi[0] - lo[0] + 3, ey = hi[1] - lo[1] + 3, ez = hi[2] - lo[2] + 3;
-  // union mode needs one cell level for the whole warp
-  int lv_lo = valid ? lv : kLevels, lv_hi = valid ? lv : -1;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    lv_lo = min(lv_lo, __shfl_xor_sync(0xffffffffu, lv_lo, off));
-    lv_hi = max(lv_hi, __shfl_xor_sync(0xffffffffu, lv_hi, off));
-  }
-  // Union of up to 128 cells, of which at most 64 non-empty: their ranges are
-  // compacted (cell order kept) into lane c % 32, slot c / 32
-  bool use_union = false;
-  int stA = 0, enA = 0, stB = 0, enB = 0, n_ne = 0;
-  if (lv_lo >= lv_hi && ex * ey * ez <= 128) {
+  if (lw >= 0) {
+    // the region's cells (x-major order), non-empty ones compacted in order
+    const unsigned long long ex = chi[0] - clo[0] + 1, ey = chi[1] - clo[1] + 1,
+                             ez = chi[2] - clo[2] + 1;
     const int ncell = (int)(ex * ey * ez);
-    for (int slot = 0; slot < 4; ++slot) {
+    int n_ne = 0;
+    int64_t mine_sz = 0;
+#pragma unroll
+    for (int slot = 0; slot < kMaxCells / 32; ++slot) {
       const int c = lane + 32 * slot;
       int st = 0, en = 0;
       if (c < ncell) {
-        const unsigned long long ix = c / (ey * ez), iy = (c / ez) % ey, iz = c % ez;
-        lookup(lo[0] - 1 + ix, lo[1] - 1 + iy, lo[2] - 1 + iz, lv_hi < 0 ? 0 : lv_hi, st, en);
+        const unsigned eyz = (unsigned)(ey * ez), ezu = (unsigned)ez, cu = (unsigned)c;
+        const unsigned ix = cu / eyz, iy = (cu / ezu) % (unsigned)ey, iz = cu % ezu;
+        lookup(clo[0] + ix, clo[1] + iy, clo[2] + iz, lw, st, en);
       }
       const unsigned ne = __ballot_sync(0xffffffffu, en > st);
       const int at = n_ne + __popc(ne & ((1u << lane) - 1u));
-      if (en > st && at < 64) {
+      if (en > st) {
         cell_st[wib][at] = st;
         cell_en[wib][at] = en;
+        mine_sz += en - st;
       }
       n_ne += __popc(ne);
     }
     __syncwarp();
-    use_union = n_ne <= 64;
-    if (use_union) {
-      if (lane < n_ne) { stA = cell_st[wib][lane]; enA = cell_en[wib][lane]; }
-      if (lane + 32 < n_ne) { stB = cell_st[wib][lane + 32]; enB = cell_en[wib][lane + 32]; }
-    }
-    __syncwarp();
-  }
-  if (use_union) {
     if (MODE == 2) {
-      int64_t tot = (int64_t)(enA - stA) + (enB - stB);
-      for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-      ub = tot;
+      for (int off = 16; off > 0; off >>= 1) mine_sz += __shfl_xor_sync(0xffffffffu, mine_sz, off);
+      ub = mine_sz;
     } else if (n_ne > 0) {
       // reference point: the first valid lane's center; every staged source
-      // and every lane center lies in the union box of ex x ey x ez cells
+      // lies within one cell of the region, every lane center in the bbox
       const int l0 = __ffs(__ballot_sync(0xffffffffu, valid)) - 1;
       const double ox = __shfl_sync(0xffffffffu, cx, l0), oy = __shfl_sync(0xffffffffu, cy, l0),
                    oz = __shfl_sync(0xffffffffu, cz, l0);
-      const double cs = prm[3] * (double)(1ull << (kSubBits + (lv_hi < 0 ? 0 : lv_hi)));
-      const double A = (double)(max(ex, max(ey, ez)) + 1) * cs;
-      run_cells(n_ne, stA, enA, stB, enB, valid, ox, oy, oz, A);
+      const double cs = prm[3] * (double)(1ull << (kSubBits + lw));
+      const double A = fmax(bhi[0] - blo[0], fmax(bhi[1] - blo[1], bhi[2] - blo[2])) + rb + 2.0 * cs;
+      run_cells(n_ne, valid, ox, oy, oz, A);
     }
-  } else {
+  } else if (any_valid) {
     // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
     // one head per distinct (cell, level): lanes of one cell need not be
     // adjacent when their levels differ
@@ -582,11 +644,16 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
         const double ox = __shfl_sync(0xffffffffu, cx, a), oy = __shfl_sync(0xffffffffu, cy, a),
                      oz = __shfl_sync(0xffffffffu, cz, a);
         const double A = 4.0 * prm[3] * (double)(1ull << (kSubBits + bl));
-        run_cells(27, st, en, 0, 0, valid && ckey == cell, ox, oy, oz, A);
+        __syncwarp();
+        if (lane < 27) {
+          cell_st[wib][lane] = st;
+          cell_en[wib][lane] = en;
+        }
+        __syncwarp();
+        run_cells(27, valid && ckey == cell, ox, oy, oz, A);
       }
     }
   }
-  if (FILL && !row && sblk && (k & 3)) sblk[32 * (k >> 2)] = pend;   // partial last block
   if (MODE == 0 && valid) cnt[g] = k;
   if (MODE == 1 && valid && cnt) cnt[g] = k;
   if (MODE == 2) {
@@ -848,14 +915,22 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
                      "no CSR entries (derive them with tsqbx_sell_to_csr)");
   char* ws = static_cast<char*>(workspace);
   int64_t* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
-  if (n_ctr > 0)
-    sweep_cell_kernel<1><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
-        ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
-        reinterpret_cast<const double4*>(ws + L.off_sxyz),
-        reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
-        reinterpret_cast<const int32_t*>(ws + L.off_hst),
-        reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, sell ? cnt : nullptr,
-        near_ptr, near_idx, sell ? sell_ptr : nullptr, sell_idx);
+  if (!sell && n_ctr > 0 && !near_idx)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_fill: no output (near_idx or sell_idx)");
+  const int nb = (int)((n_ctr + 127) / 128);
+  const double* prm = reinterpret_cast<const double*>(ws + L.off_prm);
+  const double4* sxyz = reinterpret_cast<const double4*>(ws + L.off_sxyz);
+  const auto* hkey = reinterpret_cast<const unsigned long long*>(ws + L.off_hkey);
+  const auto* hst = reinterpret_cast<const int32_t*>(ws + L.off_hst);
+  const auto* hen = reinterpret_cast<const int32_t*>(ws + L.off_hen);
+  if (n_ctr > 0 && sell)
+    sweep_cell_kernel<1><<<nb, 128, 0, st>>>(ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey,
+                                             hst, hen, L.cap, cnt, near_ptr, nullptr, sell_ptr,
+                                             sell_idx);
+  else if (n_ctr > 0)
+    sweep_cell_kernel<3><<<nb, 128, 0, st>>>(ctr_xyz, radius, n_ctr, ctr_order, prm, sxyz, hkey,
+                                             hst, hen, L.cap, nullptr, near_ptr, near_idx,
+                                             nullptr, nullptr);
   if (sell) {                           // exact lengths -> near_ptr, totals[0]
     set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
     size_t tb = L.tmp_bytes;
@@ -865,6 +940,34 @@ int tsqbx_near_fill(const double* ctr_xyz, const double* radius, int64_t n_ctr,
     if (e != cudaSuccess) return check_cuda(e, "near_fill copy");
   }
   return check_cuda(cudaGetLastError(), "near_fill launch");
+}
+
+int tsqbx_near_recount(const double* ctr_xyz, const double* radius, int64_t n_ctr, int64_t n_src,
+                       void* workspace, int64_t ws_bytes, const int32_t* ctr_order,
+                       int64_t* near_ptr, int64_t* totals, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const NearLayout L = near_layout(n_ctr, n_src);
+  if (!workspace || ws_bytes < (int64_t)L.total)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_recount: workspace too small");
+  if (!near_ptr || !totals || (n_ctr > 0 && (!ctr_xyz || !radius || !ctr_order)))
+    return set_error(TSQBX_ERR_ARGUMENT, "near_recount: null array");
+  char* ws = static_cast<char*>(workspace);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
+  if (n_ctr > 0)
+    sweep_cell_kernel<0><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+        ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
+        reinterpret_cast<const double4*>(ws + L.off_sxyz),
+        reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
+        reinterpret_cast<const int32_t*>(ws + L.off_hst),
+        reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, cnt, nullptr, nullptr, nullptr,
+        nullptr);
+  set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
+  size_t tb = L.tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(ws + L.off_tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
+  const cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t),
+                                        cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "near_recount copy");
+  return check_cuda(cudaGetLastError(), "near_recount launch");
 }
 
 int tsqbx_near_fill_rows(const double* ctr_xyz, const double* radius, int64_t n_ctr,

@@ -151,6 +151,7 @@ def check_offsets(ptr: torch.Tensor, total: int, name: str) -> None:
 
 
 _BOUND_BYTES_MAX = 16 << 30     # bound-sized SELL buffer above this: count exactly
+_COMPACT_ABOVE = 1.5            # bound slots / exact slots above this: compact the slices
 
 
 @dv.on_device
@@ -192,13 +193,13 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
         n_sell = int(totals[1].item())
         exact = n_sell * 4 > _BOUND_BYTES_MAX
         if exact:
-            # a loose bound (radii far below the cell size, e.g. C5) would need
-            # too much memory: count exactly (the sorts run again), size the
-            # slices from the exact lengths and fill them directly
-            _lib.check(L.tsqbx_near_count(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
-                                          ws.data_ptr(), ws_bytes, src_perm.data_ptr(),
-                                          ctr_order.data_ptr(), nptr.data_ptr(), None,
-                                          totals.data_ptr(), st), "tsqbx_near_count")
+            # a loose bound (union candidates far above the members, e.g. C5)
+            # would need too much memory: count exactly (reusing the sorts and
+            # the cell hash), size the slices from the exact lengths, fill them
+            _lib.check(L.tsqbx_near_recount(dv.ptr(ctr), dv.ptr(rad), n_ctr, n_src,
+                                            ws.data_ptr(), ws_bytes, ctr_order.data_ptr(),
+                                            nptr.data_ptr(), totals.data_ptr(), st),
+                       "tsqbx_near_recount")
             wsb = int(L.tsqbx_sell_workspace_bytes(n_ctr))
             sws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
             _lib.check(L.tsqbx_sell_size(n_ctr, nptr.data_ptr(), sws.data_ptr(), wsb,
@@ -227,10 +228,15 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
         _lib.check(L.tsqbx_sell_size(n_ctr, nptr.data_ptr(), sws.data_ptr(), wsb, xptr.data_ptr(),
                                      totals[1:].data_ptr(), st), "tsqbx_sell_size")
         n_pairs, n_exact = (int(v) for v in totals.tolist())
-        xidx = torch.empty(max(n_exact, 4), dtype=torch.int32, device=dev)
-        _lib.check(L.tsqbx_sell_compact(n_ctr, sptr.data_ptr(), sidx.data_ptr(), xptr.data_ptr(),
-                                        xidx.data_ptr(), st), "tsqbx_sell_compact")
-        sptr, sidx = xptr, xidx
+        if n_sell > _COMPACT_ABOVE * n_exact:
+            xidx = torch.empty(max(n_exact, 4), dtype=torch.int32, device=dev)
+            _lib.check(L.tsqbx_sell_compact(n_ctr, sptr.data_ptr(), sidx.data_ptr(),
+                                            xptr.data_ptr(), xidx.data_ptr(), st),
+                       "tsqbx_sell_compact")
+            sptr, sidx = xptr, xidx
+        # else: the bound-sized slices are kept as they are -- every index was
+        # written once, the kernels never read a slot past a row's length, and
+        # the DRAM index stream is the same (a row's blocks stay contiguous)
     return NearLists(n_ctr=n_ctr, n_src=n_src, n_pairs=n_pairs, ptr=nptr,
                      csr_idx=None if idx is None else idx[:n_pairs],
                      src_perm=src_perm[:n_src], ctr_order=ctr_order[:n_ctr],
