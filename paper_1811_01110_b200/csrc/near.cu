@@ -336,6 +336,11 @@ constexpr int kMaxCells = 128;   // cells one union pass stages (non-empty ones)
 #define TSQBX_WALK_ABOVE 20
 #endif
 constexpr unsigned kWalkAbove = TSQBX_WALK_ABOVE;
+// SELL fill: 16-byte block stores (1) or one 4-byte store per entry (0)
+#ifndef TSQBX_INT4_STORES
+#define TSQBX_INT4_STORES 1
+#endif
+constexpr bool kInt4Stores = TSQBX_INT4_STORES != 0;
 
 // MODE 0: count members per row; 1: fill the SELL column (plus the row length
 // when `cnt` is given); 3: fill the CSR row; 2: bound -- no distance tests, the
@@ -385,6 +390,7 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
   int32_t* dst = (MODE == 3 && valid) ? nidx + nptr[g]
                  : (MODE == 1 && valid) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
   int k = 0;
+  int4 pend = make_int4(0, 0, 0, 0);   // MODE 1 with kInt4Stores: the row's open block
   int64_t ub = 0;                      // MODE 2: candidates this row will test
   // Stage the sources of a list of up to kMaxCells cells (ranges [st, en) in
   // cell_st / cell_en of this warp, written by the caller) through the tile;
@@ -499,7 +505,17 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
             // (every lane stores its own) beats a per-lane loop that runs as
             // long as the busiest lane
             auto put = [&](int j) {
-              dst[MODE == 3 ? k : ((k >> 2) << 7) | (k & 3)] = j;
+              if (MODE == 3 || !kInt4Stores) {
+                dst[MODE == 3 ? k : ((k >> 2) << 7) | (k & 3)] = j;
+              } else {
+                // SELL: the row's current block as a 4-entry shift register,
+                // one 16-byte store per completed block
+                pend.x = pend.y;
+                pend.y = pend.z;
+                pend.z = pend.w;
+                pend.w = j;
+                if ((k & 3) == 3) *reinterpret_cast<int4*>(dst + ((k >> 2) << 7)) = pend;
+              }
               ++k;
             };
             // (only the lanes testing this list are active here: per-cell mode)
@@ -653,6 +669,14 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
         run_cells(27, valid && ckey == cell, ox, oy, oz, A);
       }
     }
+  }
+  if (MODE == 1 && kInt4Stores && valid && (k & 3)) {   // the last, partial block
+    const int r = k & 3;                                // entries pending in pend's tail
+    int4 blk = pend;
+    if (r == 1) blk.x = pend.w;
+    if (r == 2) { blk.x = pend.z; blk.y = pend.w; }
+    if (r == 3) { blk.x = pend.y; blk.y = pend.z; blk.z = pend.w; }
+    *reinterpret_cast<int4*>(dst + ((k >> 2) << 7)) = blk;
   }
   if (MODE == 0 && valid) cnt[g] = k;
   if (MODE == 1 && valid && cnt) cnt[g] = k;
