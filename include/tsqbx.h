@@ -67,6 +67,11 @@ extern "C" {
 /* a performance hint: the near lists are long (mean >~ 48 entries), pick the
  * kernel builds tuned for long rows (never changes results) */
 #define TSQBX_FLAG_LONG_ROWS (1u << 16)
+/* Laplace S with uniform target runs of 1 or 2 (TSQBX_FLAG_UNIFORM_TARGETS)
+ * and the CSR entries (near_idx) given: evaluate with the short-list kernel
+ * (a warp's 32 rows' entries split evenly over its lanes) instead of the
+ * SELL thread-per-row kernel -- for near lists of a few dozen sources. */
+#define TSQBX_FLAG_FLAT (1u << 17)
 
 #define TSQBX_MAX_ORDER 64
 

@@ -642,7 +642,11 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   const int nt = (flags & TSQBX_FLAG_ONE_TARGET) ? 1
                  : (flags & TSQBX_FLAG_UNIFORM_TARGETS) ? (a.tuni >= 2 ? 2 : 1)
                  : (n_tgt >= 2 * n_ctr ? 2 : 1);
-  if (fast) {
+  const bool flat = fast && equation == TSQBX_EQ_LAPLACE && (flags & TSQBX_FLAG_FLAT) &&
+                    near_idx && (flags & TSQBX_FLAG_UNIFORM_TARGETS) && a.tuni <= 2;
+  if (flat) {
+    launch_laplace_flat(p, a.tuni, val, a, n_ctr, st);
+  } else if (fast) {
     (equation == TSQBX_EQ_LAPLACE ? launch_laplace_fast : launch_helmholtz_fast)(
         p, sell_ptr != nullptr, nt, val, a, n_ctr, st);
   } else if (fast_deriv) {

@@ -296,6 +296,8 @@ bool launch_laplace_fast(int p, bool sell, int nt, bool val, const EvalParams& a
                          cudaStream_t st);
 bool launch_helmholtz_fast(int p, bool sell, int nt, bool val, const EvalParams& a,
                            int64_t n_ctr, cudaStream_t st);
+bool launch_laplace_flat(int p, int nt, bool val, const EvalParams& a, int64_t n_ctr,
+                         cudaStream_t st);
 bool launch_deriv_fast(int p, int equation, int variant, int nt, const EvalParams& a,
                        int64_t n_ctr, cudaStream_t st);
 

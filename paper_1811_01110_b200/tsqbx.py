@@ -79,6 +79,23 @@ def pick_split(mean_len: float, n_rows: int, one_target: bool, sms: int = 148,
     return 4 if waves < 1.5 else 2
 
 
+# Mean near-list length below which Laplace S would take the short-list kernel
+# (laplace_flat_kernel: a warp's 32 rows' CSR entries split evenly over its
+# lanes).  0 = never: measured slower than the SELL thread-per-row kernel on
+# every literal preset (C2 literal 34.0 vs 27.3 us, C4 literal 74.7 vs 50.0 us;
+# ncu: the same FP64 work, 35 % more instructions, 24 instead of 32 warps per
+# SM at NT = 2) -- the literal presets are not limited by lane divergence.
+FLAT_BELOW = 0.0
+
+
+def pick_flat(mean_len: float) -> bool:
+    """Whether Laplace S takes the short-list kernel; GIGAQBX_FLAT=0/1 overrides."""
+    env = os.environ.get("GIGAQBX_FLAT")
+    if env is not None:
+        return env == "1"
+    return mean_len < FLAT_BELOW
+
+
 def pick_layout() -> str:
     """'sell' (thread per center on the sliced-ELL copy, the default) or 'csr'
     (groups of lanes per center on the CSR rows); GIGAQBX_LAYOUT overrides."""
@@ -172,6 +189,7 @@ class _Prepared:
         self.real_w = False
         self.one_target = os.environ.get("GIGAQBX_ONE_TARGET", "0") == "1"
         self.tuni = 0         # k > 0: every row owns k consecutive targets (set_uniform_targets)
+        self.flat = False     # Laplace S, uniform runs of 1-2 targets, short lists: flat kernel
         self._auto_split = (not group_lanes and self.layout == "sell" and spec.is_laplace
                             and self.variant == 0 and "GIGAQBX_SPLIT" not in os.environ)
         # Helmholtz: every near source lies within the largest near radius, so
@@ -193,6 +211,9 @@ class _Prepared:
         if known or bool(torch.equal(self.tptr, torch.arange(
                 self.n_ctr + 1, dtype=torch.int64, device=self.dev) * k)):
             self.tuni = k
+            self.flat = (k <= 2 and self.layout == "sell" and self.cfg.spec.is_laplace
+                         and self.variant == 0 and self.cfg.p_qbx <= 16
+                         and pick_flat(self.near.mean_len))
             if self._auto_split:          # the uniform kernel fits one more CTA per SM
                 self.G = pick_split(self.near.mean_len, self.n_ctr, k == 1,
                                     dv.sm_count(self.dev.index if self.dev.index is not None
@@ -239,7 +260,10 @@ class _Prepared:
             raise ValueError("row ranges on the SELL layout must start at a multiple of 32")
         # the fast S kernels read only the SELL copy; the others need the CSR entries
         fast = self.cfg.p_qbx <= 16 and not generic
-        csr = None if (sell and fast) else near.idx
+        flat = self.flat and fast
+        if flat:
+            flags |= _lib.FLAG_FLAT
+        csr = None if (sell and fast and not flat) else near.idx
         _lib.check(L.tsqbx_eval_packed(
             self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,
             self.with_normals, self.ctr.data_ptr() + 24 * g0, g1 - g0,

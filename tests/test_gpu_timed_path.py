@@ -54,8 +54,10 @@ def _expected_instance(case, prob):
     assert prob.prep.tuni == tpc, (prob.prep.tuni, tpc)
     if case.cfg.spec.is_laplace:
         assert prob.group_lanes == (1 if case.preset == "literal" else 2)
+        assert not prob.prep.flat          # the short-list kernel is opt-in (GIGAQBX_FLAT=1)
     else:
         assert prob.group_lanes == 1
+        assert not prob.prep.flat
 
 
 def _oracle(case, uptr, uidx, sel=None):
