@@ -43,6 +43,11 @@ constexpr int kP2PBlock = 128;   // threads per CTA == sources per shared tile
 #define TSQBX_P2P_TPT 4
 #endif
 constexpr int kP2PTpt = TSQBX_P2P_TPT;   // targets per thread on large dense sums
+// Helmholtz e^{ikr}: Cody-Waite reduction + the near-minimax pair (sincos_cw)
+// instead of the library sincos
+#ifndef TSQBX_P2P_CW
+#define TSQBX_P2P_CW 1
+#endif
 
 struct P2PParams {
   const double4* __restrict__ sp;     // {x, y, z, Re w}
@@ -91,7 +96,11 @@ struct PairKernel {
     } else {
       const double r = r2 * rinv;
       double s, co;
+#if TSQBX_P2P_CW
+      sincos_cw(k * r, s, co);
+#else
       sincos(k * r, &s, &co);
+#endif
       if (VARIANT == TSQBX_VARIANT_S) {
         // w e^{ikr} / r (_core.pyx:151-152)
         const double pr = co * rinv, pi = s * rinv;
