@@ -329,6 +329,43 @@ def cpu_reference_rate(case, seconds, processes=1, n_sample=200000):
         ref.close()
 
 
+def cpu_public_api_rate(case, seconds, n_sample=20000):
+    """The reference's PUBLIC per-call API: its own
+    ``gigaqbx.tsqbx.ts_accumulate`` (``_prep`` validation + the compiled
+    backend, tsqbx.py:68-80) per (center, target) on one core, from the
+    unmodified install in baseline/_ref.  None when that install is absent."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "gigaqbx")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    from gigaqbx import kernels as rk, tsqbx as rt
+    from gigaqbx._backend import BACKEND_NAME
+    spec = case.cfg.spec
+    rspec = rk.KernelSpec(equation=rk.Equation(spec.equation.value),
+                          variant=rk.Variant(spec.variant.value), helmholtz_k=spec.helmholtz_k)
+    cfg = rt.TsConfig(rspec, case.cfg.p_qbx)
+    sel = sample_centers(case, n_sample, seed=321)
+    ptr, idx, tptr, tsel = cpu_sample_problem(case, sel)
+    pairs, n_done = 0, 0
+    t0 = time.perf_counter()
+    for i, c in enumerate(sel):
+        rows = idx[ptr[i]:ptr[i + 1]]
+        src, w = case.sources[rows], case.weights[rows]
+        for t in tsel[tptr[i]:tptr[i + 1]]:
+            rt.ts_accumulate(cfg, src, w, case.centers[c], case.targets[t])
+            pairs += len(rows)
+        n_done = i + 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": pairs / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{n_done} seeded-random centers of {case.n_centers} ({pairs} pairs), the "
+                      f"reference's public gigaqbx.tsqbx.ts_accumulate per (center, target) "
+                      f"(_prep + backend '{BACKEND_NAME}', baseline/_ref), 1 process, {dt:.2f} s; "
+                      f"host CPU: {cpu_model()}"}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def main_reference(args):
     """The reference arm: the reference's own CPU implementation of the path on
@@ -379,9 +416,18 @@ def main_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
-def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
-    """Device-resident kernel throughput for one case."""
-    from paper_1811_01110_b200 import TsqbxProblem, build_near_lists, configs
+def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0, variant=None):
+    """Device-resident kernel throughput for one case (``variant``: evaluate the
+    S' or D layer potential of the same geometry instead of S; normals are the
+    sources' surface normals, a target takes its center's)."""
+    from paper_1811_01110_b200 import KernelSpec, TsConfig, TsqbxProblem, build_near_lists, configs
+    cfg, extra = case.cfg, {}
+    if variant is not None:
+        sp = case.cfg.spec
+        cfg = TsConfig(KernelSpec(equation=sp.equation, variant=variant,
+                                  helmholtz_k=sp.helmholtz_k), case.cfg.p_qbx)
+        extra = {"source_normals": case.normals,
+                 "target_normals": np.repeat(case.normals, np.diff(case.tgt_ptr), axis=0)}
     # device near-list build, steady state: geometry already in HBM, second build
     # (the first one pays the allocator's cudaMalloc calls)
     ctr_d = torch.as_tensor(case.centers, device=dev)
@@ -397,8 +443,9 @@ def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
     torch.cuda.synchronize()
     csr_ms = e0.elapsed_time(e1)
     del ctr_d, src_d, rad_d
-    prob = TsqbxProblem(case.cfg, case.sources, case.weights, case.centers, case.targets, near,
-                        tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev)
+    prob = TsqbxProblem(cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr, group_lanes=args.group_lanes or None, device=dev,
+                        **extra)
     pairs = prob.pair_count()
     for _ in range(max(3, args.warmup)):
         prob.evaluate()
@@ -416,8 +463,8 @@ def measure_case(torch, case, args, dev, flush, want_clocks=False, index=0):
         clocks = sampler.summary()
     else:
         ms = time_device_steps(torch, prob.evaluate, args.steps, flush)
-    spec = case.cfg.spec
-    fpp = configs.algorithmic_flops_per_pair(spec, case.cfg.p_qbx)
+    spec = cfg.spec
+    fpp = configs.algorithmic_flops_per_pair(spec, cfg.p_qbx)
     mean_ms = sum(ms) / len(ms)
     launches_per_step = 1   # one evaluation kernel (Helmholtz SELL computes j_n in-kernel)
     # SURVEY.md 8(d) compulsory bytes: sources 40 B, centers 32 B, 4 B per CSR entry,
@@ -632,7 +679,8 @@ def main_ours(args):
                              "achieved_gbs": res["alg_bytes"] / (res["mean_ms"] * 1e-3) / 1e9,
                              "peak_gbs": HBM_PEAK,
                              "note": "HBM is not the bound: flop/byte >> ridge ~5.5"},
-                     "flops_convention": "algorithmic, SURVEY.md 8(d): Laplace 7p+17, "
+                     "flops_convention": "algorithmic, SURVEY.md 8(d) (configs.algorithmic_flops_per_pair): "
+                                         "Laplace S 7p+17, "
                                          "Helmholtz 14p+30 per pair"},
         "gpu_launches": res["launches_per_step"] * args.steps,
         "clocks": clocks,
@@ -706,6 +754,9 @@ def main_ours(args):
         rate, cores, kind, sample = cpu_reference_rate(case, args.cpu_seconds, processes=1)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                                 "sample": sample, "cpu_model": cpu_model()}
+        pub = cpu_public_api_rate(case, min(args.cpu_seconds, 8.0))
+        if pub is not None:
+            line["cpu_baseline_public_api"] = pub
     if not args.no_secondary:
         sec = {}
         for name, preset in (("c2", "dense"), ("c2", "literal"), ("c3", "dense"),
@@ -724,6 +775,22 @@ def main_ours(args):
             del p2
             torch.cuda.empty_cache()
         line["secondary"] = sec
+        # S' and D (row f1) on the C2 / C3 dense geometry: same lists, algorithmic
+        # flops per pair of configs.algorithmic_flops_per_pair
+        from paper_1811_01110_b200.kernels import Variant
+        var = {}
+        for name in ("c2", "c3"):
+            c2 = configs.make_case(name, "dense")
+            for vname, v in (("S'", Variant.TARGET_NORMAL_DERIV),
+                             ("D", Variant.SOURCE_NORMAL_DERIV)):
+                r, p2, _ = measure_case(torch, c2, args, dev, flush, variant=v)
+                var[f"{name}/dense/{vname}"] = {
+                    "value": r["value"], "ms_per_step": r["mean_ms"],
+                    "flops_per_pair": r["flops_per_pair"], "tflops": r["tflops"],
+                    "roofline_frac": r["tflops"] / peak if peak else None}
+                del p2
+                torch.cuda.empty_cache()
+        line["variants"] = var
         line["p2p"] = measure_p2p(torch, dev, flush, peak)
         line["direct_stage"] = measure_direct_stage(torch, dev, flush)
     print(json.dumps(line))

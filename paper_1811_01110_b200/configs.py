@@ -163,8 +163,34 @@ def _spheres_case(n_per, count, preset, seed):
 
 
 def algorithmic_flops_per_pair(spec: KernelSpec, p: int) -> int:
-    """Laplace S 7p + 17, Helmholtz S 14p + 30."""
-    return 7 * p + 17 if spec.is_laplace else 14 * p + 30
+    """Algorithmic flops per (target, near source) pair, SURVEY.md 8(d)'s
+    convention (add/sub/mul 1, FMA 2, sqrt/rsqrt/div/sin/cos 1; per-target work
+    -- t - c, r, t-hat, n_t . t-hat, j_n(kr) and its scaled tables, the 1/(4 pi)
+    or ik/(4 pi) factor -- excluded):
+
+    * Laplace S   7p + 17 (_core.pyx:229-259).
+    * Laplace S'  12p + 22 (_core.pyx:260-282): the S geometry (s - c 3, R^2 5,
+      1/R 1, cos g 6, rho 1 = 16); n_t . s-hat 6; (n_t.s-hat - n_t.t-hat cos g) 2;
+      1/R^2 1; per order n = 1..p the term radial (n n_t.t-hat P_n + X P'_n),
+      s += : 5p; for n < p Legendre 4, P' ladder 2, radial *= rho 1: 7(p - 1);
+      complex-weight accumulate 4.
+    * Laplace D   13p + 29 (_core.pyx:283-304): geometry 16; n_s . s-hat 6;
+      n_s . t-hat 5; (n_s.t-hat - n_s.s-hat cos g) 2; 1/R^2 1; n = 0 term 1;
+      per order radial *= rho and -(n+1) n_s.s-hat P_n + Y P'_n, s += : 7p;
+      Legendre + P' ladder for n < p: 6(p - 1); accumulate 4.
+    * Helmholtz S 14p + 30 (_core.pyx:363-398).
+    * Helmholtz S' 19p + 37 (_core.pyx:399-407): the S terms with the
+      derivative ladder 2(p - 1), n_t . s-hat 6, (n_t.s-hat - n_t.t-hat cos g) 2,
+      and 8 instead of 5 flops per order for h_n (a_n P_n + X b_n P'_n).
+    * Helmholtz D 27p + 50 (_core.pyx:408-416): the S terms with the derivative
+      ladder 2(p - 1), h'_n = h_{n-1} - (n+1)/x h_n 4p, n_s . s-hat 6,
+      n_s . t-hat 5, Y 2, k n_s.s-hat 1, Y/R 1, and 12 instead of 5 flops per
+      order for c_n (k n_s.s-hat h'_n P_n + (Y/R) h_n P'_n).
+    """
+    v = spec.variant_code
+    if spec.is_laplace:
+        return (7 * p + 17, 12 * p + 22, 13 * p + 29)[v]
+    return (14 * p + 30, 19 * p + 37, 27 * p + 50)[v]
 
 
 def synthetic_box_tree(case, conv, cell):
