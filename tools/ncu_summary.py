@@ -56,9 +56,9 @@ def load(path):
                     f *= 1e9
                 elif m.startswith("dram__bytes") and unit == "Kbyte":
                     f *= 1e3
-                if m == "gpu__time_duration.sum" and unit == "msecond":
+                if m == "gpu__time_duration.sum" and unit in ("msecond", "ms"):
                     f *= 1e3
-                elif m == "gpu__time_duration.sum" and unit == "nsecond":
+                elif m == "gpu__time_duration.sum" and unit in ("nsecond", "ns"):
                     f *= 1e-3
                 rec[k] = f
             except ValueError:
