@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 9
+#define TSQBX_ABI_VERSION 10
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -216,6 +216,31 @@ int tsqbx_near_recount(const double* ctr_xyz, const double* radius, int64_t n_ct
                        int64_t n_src, void* workspace, int64_t ws_bytes,
                        const int32_t* ctr_order, int64_t* near_ptr, int64_t* totals,
                        void* stream);
+/* The bounding box, Morton sorts (src_perm, ctr_order) and cell hash of
+ * tsqbx_near_count without any sweep: the state tsqbx_eval_fused reads. */
+int tsqbx_near_index(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                     const double* src_xyz, int64_t n_src, void* workspace, int64_t ws_bytes,
+                     int32_t* src_perm, int32_t* ctr_order, void* stream);
+/* One-shot near field (Laplace / Helmholtz S, compile-time p <= 16, uniform
+ * target runs of 1 or 2 per center): every warp sweeps the near lists of 32
+ * consecutive rows into a per-warp scratch slice and evaluates them at once;
+ * no CSR is materialised.  After tsqbx_near_index on (ctr_user, radius,
+ * sources) with `near_ws`; packed = tsqbx_pack_sources with src_perm;
+ * ctr_proc / tgt_proc / tgt_out from tsqbx_order_targets.  flags:
+ * TSQBX_FLAG_UNIFORM_TARGETS (| k << 8) required, VALIDATE / REAL_WEIGHTS /
+ * KR_* as for tsqbx_eval_packed.  err: device int64[2] -- err[0] the
+ * validation key, err[1] != 0 when a row had more than row_cap near sources
+ * (the caller evaluates through tsqbx_near_count/fill + tsqbx_eval_packed
+ * instead).  scratch: tsqbx_fused_scratch_bytes(equation, p, k, validate,
+ * row_cap) bytes (sized by the resident CTAs of the current device). */
+int64_t tsqbx_fused_scratch_bytes(int equation, int p, int targets_per_center, int validate,
+                                  int row_cap);
+int tsqbx_eval_fused(int equation, double k, int p, const double* packed, int64_t n_src,
+                     const double* ctr_user, const double* radius, const int32_t* ctr_order,
+                     void* near_ws, int64_t near_ws_bytes, const double* ctr_proc, int64_t n_ctr,
+                     const double* tgt_proc, int64_t n_tgt, const int64_t* tgt_out,
+                     unsigned flags, int row_cap, void* scratch, int64_t scratch_bytes,
+                     double* out, int64_t* err, void* stream);
 /* Rows g0..g1-1 of the processing order only (a rank's shard),
  * SELL mode: after tsqbx_near_count over ALL centers (CSR mode: exact row
  * lengths), the caller sizes the shard's slices from near_ptr[g0..g1] (e.g.

@@ -12,14 +12,14 @@ from ._backend import BACKEND_NAME, available_backends, get_backend
 from .kernels import Equation, KernelSpec, Variant
 from .nearlist import NearLists, build_near_lists
 from .p2p import P2PProblem, direct_sum, kernel_value, p2p_rows
-from .tsqbx import (PendingPotentials, TsConfig, TsqbxProblem, ts_accumulate,
-                    ts_accumulate_batch, ts_eval)
+from .tsqbx import (PendingPotentials, TsConfig, TsqbxProblem, near_field_potentials,
+                    ts_accumulate, ts_accumulate_batch, ts_eval)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BACKEND_NAME", "available_backends", "get_backend", "Equation", "KernelSpec", "Variant",
     "NearLists", "build_near_lists", "TsConfig", "TsqbxProblem", "ts_accumulate",
-    "ts_accumulate_batch", "ts_eval", "PendingPotentials", "P2PProblem", "direct_sum",
+    "ts_accumulate_batch", "ts_eval", "near_field_potentials", "PendingPotentials", "P2PProblem", "direct_sum",
     "kernel_value", "p2p_rows", "__version__",
 ]

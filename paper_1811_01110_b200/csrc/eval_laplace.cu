@@ -1,6 +1,6 @@
 // eval_laplace.cu -- Laplace S kernels (compile-time order P <= 16): the
 // SELL-32x4 thread-per-row kernel (the hot path) and the CSR group kernel.
-#include "eval_kernels.cuh"
+#include "eval_bodies.cuh"
 
 namespace tsqbx {
 
@@ -67,86 +67,6 @@ __global__ void __launch_bounds__(256) laplace_s_kernel(const EvalParams a) {
       }
     }
   }
-}
-
-template <int P, int NT, bool VAL, bool REALW, int S = 1>
-__device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g,
-                                                  const RowHead& h, int4* ring, int part = 0,
-                                                  unsigned gmask = 0xffffffffu) {
-  const double cx = h.cx, cy = h.cy, cz = h.cz;
-  const int len = h.len;
-  const int64_t t0 = h.t0, t1 = h.t1;
-  // high orders have more arithmetic per source to cover a second gather in
-  // flight (measured: C4 literal p = 12 +7 %; p = 8 -2 %); split rows (S > 1,
-  // the dense presets) keep one in flight (C4 dense +2.2 %)
-  using Stream = SellStream<false, (P >= 12 && S == 1 ? 2 : TSQBX_GATHER_DEPTH)>;
-  // the index ring starts filling before the target range is known
-  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S);
-  for (int64_t tb = t0; tb < t1; tb += NT) {
-    double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];
-    // VAL: min |s-c|^2 over the row as its IEEE bit pattern (R^2 >= 0, so the
-    // integer order is the numeric order): integer-pipe min, screen r^2 > R^2
-    long long rmin = 0x7ff0000000000000ll;
-    int64_t slot[NT];   // output slots, loaded up front so the epilogue does not wait
-#pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      const bool ok = tb + q < t1;
-      slot[q] = ok ? out_slot(a, tb + q) : 0;
-      tx[q] = ok ? a.tgt[3 * (tb + q)] - cx : 0.0;
-      ty[q] = ok ? a.tgt[3 * (tb + q) + 1] - cy : 0.0;
-      tz[q] = ok ? a.tgt[3 * (tb + q) + 2] - cz : 0.0;
-      r2[q] = fma(tz[q], tz[q], fma(ty[q], ty[q], tx[q] * tx[q]));
-      ar[q] = ai[q] = 0.0;
-    }
-    if (tb == t0) ss.start();
-    else ss.restart();
-    // one source against the NT targets
-    auto source = [&](const double4& q4, double wim) {
-      const double dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
-      const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const double iR = rsqrt_fast(R2);
-      const double iR2 = iR * iR;
-      const double wr = q4.w * iR;
-      const double wi = REALW ? 0.0 : wim * iR;
-      if (VAL) rmin = min(rmin, __double_as_longlong(R2));
-#pragma unroll
-      for (int q = 0; q < NT; ++q) {
-        const double A = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR2;
-        const double B = r2[q] * iR2;
-        const double ser = laplace_series<P>(A, B);
-        ar[q] = fma(ser, wr, ar[q]);
-        if (!REALW) ai[q] = fma(ser, wi, ai[q]);
-      }
-    };
-    while (ss.more()) {
-      double4 q4;
-      double wim;
-      ss.next(q4, wim);
-      source(q4, wim);
-    }
-    if (S > 1) {
-      // the S threads of this row hold partial sums over interleaved blocks:
-      // a fixed xor tree over the part bits (lanes 32/S apart) adds them
-#pragma unroll
-      for (int off = 32 / S; off < 32; off <<= 1) {
-#pragma unroll
-        for (int q = 0; q < NT; ++q) {
-          ar[q] += __shfl_xor_sync(gmask, ar[q], off);
-          if (!REALW) ai[q] += __shfl_xor_sync(gmask, ai[q], off);
-        }
-        if (VAL) rmin = min(rmin, __shfl_xor_sync(gmask, rmin, off));
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      if (tb + q < t1 && part == 0) {
-        a.out[slot[q]] = make_double2(ar[q] * kInvFourPi, ai[q] * kInvFourPi);
-        if (VAL && (!isfinite(ar[q]) || !isfinite(ai[q]) || r2[q] > kSepScreen * __longlong_as_double(rmin)))
-          flag_suspect(a.err);
-      }
-    }
-  }
-  if (t0 >= t1) cp_async_wait<0>();   // no pass consumed the ring: drain it before exit
 }
 
 // real weights (the usual Laplace density) skip every Im w load and FMA; the

@@ -450,18 +450,106 @@ def _deliver(out_dev: torch.Tensor, out, host_out: bool):
     return out_dev.cpu().numpy() if host_out else out_dev
 
 
+FUSED_ROW_CAP = 1024     # near sources per row the fused kernel's scratch slice holds
+
+
+def _uniform_run(tgt_ptr, n_ctr: int, n_tgt: int, dev) -> int:
+    """k when every center owns k consecutive targets (tgt_ptr = k * arange), else 0."""
+    if tgt_ptr is None:
+        return 1 if n_tgt == n_ctr else 0
+    k = n_tgt // n_ctr if n_ctr else 0
+    if not (1 <= k <= 2 and k * n_ctr == n_tgt):
+        return 0
+    if isinstance(tgt_ptr, torch.Tensor):
+        ok = bool(torch.equal(tgt_ptr.to(device=dev, dtype=torch.int64),
+                              torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) * k))
+    else:
+        ok = bool(np.array_equal(np.asarray(tgt_ptr), np.arange(n_ctr + 1) * k))
+    return k if ok else 0
+
+
+def _fused_potentials(cfg: TsConfig, dev, src, w, ctr, rad, tgt, k_run: int, validate: bool,
+                      row_cap: int):
+    """One-shot near field through tsqbx_eval_fused (csrc/fused.cu): Morton sorts
+    and cell hash (tsqbx_near_index), then one kernel that sweeps every warp's 32
+    rows into a scratch slice and evaluates them -- no CSR in HBM.  Returns the
+    potentials (CUDA, user order) or None when a row overflowed the scratch slice
+    or the validation screen fired (the caller takes the two-step path, which
+    names the offending source exactly)."""
+    L = _lib.load()
+    st = dv.stream_handle(dev)
+    spec = cfg.spec
+    n_src, n_ctr, n_tgt = int(src.shape[0]), int(ctr.shape[0]), int(tgt.shape[0])
+    eq = _equation_code(spec)
+    sb = int(L.tsqbx_fused_scratch_bytes(eq, cfg.p_qbx, k_run, int(validate), row_cap))
+    if sb < 0:
+        return None
+    wsb = int(L.tsqbx_near_workspace_bytes(n_ctr, n_src))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    src_perm = torch.empty(max(n_src, 1), dtype=torch.int32, device=dev)
+    ctr_order = torch.empty(max(n_ctr, 1), dtype=torch.int32, device=dev)
+    _lib.check(L.tsqbx_near_index(ctr.data_ptr(), rad.data_ptr(), n_ctr, src.data_ptr(), n_src,
+                                  ws.data_ptr(), wsb, src_perm.data_ptr(), ctr_order.data_ptr(),
+                                  st), "tsqbx_near_index")
+    nd = int(L.tsqbx_packed_doubles(n_src, 0))
+    packed = torch.empty(max(nd, 4), dtype=torch.float64, device=dev)
+    _lib.check(L.tsqbx_pack_sources(n_src, src.data_ptr(), w.data_ptr(), None,
+                                    src_perm.data_ptr(), packed.data_ptr(), st),
+               "tsqbx_pack_sources")
+    tptr = torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) * k_run
+    ctr_p, tptr_p, tgt_p = torch.empty_like(ctr), torch.empty_like(tptr), torch.empty_like(tgt)
+    tidx = torch.empty(max(n_tgt, 1), dtype=torch.int64, device=dev)
+    owb = int(L.tsqbx_order_workspace_bytes(n_ctr))
+    ows = torch.empty(max(owb, 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.tsqbx_order_targets(n_ctr, ctr_order.data_ptr(), ctr.data_ptr(), tptr.data_ptr(),
+                                     tgt.data_ptr(), None, n_tgt, ows.data_ptr(), owb,
+                                     ctr_p.data_ptr(), tptr_p.data_ptr(), tgt_p.data_ptr(), None,
+                                     tidx.data_ptr(), None, st), "tsqbx_order_targets")
+    flags = (_lib.FLAG_UNIFORM_TARGETS | (k_run << 8)
+             | (_lib.FLAG_VALIDATE if validate else 0))
+    if not spec.is_laplace:
+        # every member lies within the largest radius: one sin/cos series, no vote
+        kr = float(spec.helmholtz_k) * float(rad.max().item()) * (1.0 + 1e-12)
+        flags |= (_lib.FLAG_KR_NARROW if kr <= math.pi / 4 else
+                  _lib.FLAG_KR_WIDE if kr <= math.pi / 2 else 0)
+    scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    err = torch.empty(2, dtype=torch.int64, device=dev)
+    res = torch.empty(n_tgt, dtype=torch.complex128, device=dev)
+    _lib.check(L.tsqbx_eval_fused(eq, float(spec.helmholtz_k or 0.0), cfg.p_qbx,
+                                  packed.data_ptr(), n_src, ctr.data_ptr(), rad.data_ptr(),
+                                  ctr_order.data_ptr(), ws.data_ptr(), wsb, ctr_p.data_ptr(),
+                                  n_ctr, tgt_p.data_ptr(), n_tgt, tidx.data_ptr(), flags,
+                                  row_cap, scratch.data_ptr(), sb,
+                                  torch.view_as_real(res).data_ptr(), err.data_ptr(), st),
+               "tsqbx_eval_fused")
+    key, overflow = err.tolist()
+    if overflow or (validate and key != _lib.ERR_KEY_NONE):
+        return None
+    return res
+
+
 @dv.on_device
 def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, targets,
                           tgt_ptr=None, source_normals=None, target_normals=None,
                           validate: bool = True, group_lanes: int | None = None, device=None,
-                          out=None):
+                          out=None, fused: bool | None = None):
     """The whole near-field path in one call: geometry -> device radius-ball near
-    lists (``build_near_lists``) -> TSQBX evaluation -> per-target potentials.
+    lists -> TSQBX evaluation -> per-target potentials.
 
     Host inputs are copied to the device once (asynchronously when they are
     pinned tensors); the result comes back as numpy, into ``out`` (e.g. a
     pinned complex128 tensor) when given, or stays a CUDA tensor when
-    ``sources`` is one."""
+    ``sources`` is one.
+
+    ``fused=True`` (or GIGAQBX_FUSED=1; S, p <= 16, one or two targets per
+    center in runs, no ``group_lanes``): the near lists are swept and evaluated
+    in one kernel without a CSR in HBM (``tsqbx_eval_fused``); a row with more
+    than FUSED_ROW_CAP sources or a flagged validation screen re-runs through
+    ``build_near_lists`` + the evaluation kernels, which also raise the
+    reference's ValueError.  Off by default: measured slower than the two-step
+    path (C5 dense 48.7 vs 41.5 ms end to end -- the fused kernel's sweep and
+    evaluation phases do not overlap on an SM, 26.5 ms against 27 ms for the
+    count, fill and evaluation kernels)."""
     from .nearlist import build_near_lists
 
     host_out = not (isinstance(sources, torch.Tensor) and sources.is_cuda)
@@ -483,6 +571,25 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
                                        target_normals, dev)
         tptr = (torch.arange(n_ctr + 1, dtype=torch.int64, device=dev) if tgt_ptr is None
                 else dv.to_device(tgt_ptr, torch.int64, dev))
+    if fused is None:
+        fused = os.environ.get("GIGAQBX_FUSED", "0") == "1"
+    fused = (fused and cfg.spec.variant_code == 0 and cfg.p_qbx <= 16 and not group_lanes
+             and n_ctr > 0)
+    if fused:
+        main.wait_stream(side)
+        for t in (w, tgt, tptr):
+            if t is not None:
+                t.record_stream(main)
+        if tgt_ptr is None and int(tgt.shape[0]) != n_ctr:
+            raise ValueError("tgt_ptr is required unless there is one target per center")
+        k_run = _uniform_run(tgt_ptr, n_ctr, int(tgt.shape[0]), dev)
+        if k_run:
+            row_cap = int(os.environ.get("GIGAQBX_FUSED_ROW_CAP", FUSED_ROW_CAP))
+            radc = (rad.reshape(-1).expand(n_ctr) if rad.numel() == 1 else rad.reshape(-1))
+            res = _fused_potentials(cfg, dev, src, w, ctr, radc.contiguous(), tgt, k_run,
+                                    validate, row_cap)
+            if res is not None:
+                return _deliver(res, out, host_out)
     near = build_near_lists(ctr, src, rad, dev)
     main.wait_stream(side)
     for t in (w, tgt, sn, tn, tptr):
