@@ -162,7 +162,7 @@ __device__ __forceinline__ void helmholtz_sell_row(const EvalParams& a, int64_t 
       const double invx = iR * invk;
       double hmr, hmi, hcr, hci;                 // h_{n-1}, h_n
       hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci, a.series);
-      double cg[NT], pm[NT], pc[NT], sr[NT], si[NT];
+      double cg[NT], sr[NT], si[NT];
       if constexpr (kClenshaw) {
         // sum_n a_n h_n, a_n = c_n P_n(cos g) real, by Clenshaw over the Hankel
         // recurrence h_{n+1} = (2n+1) u h_n - h_{n-1} (u = 1/x, _core.pyx:192-193):
@@ -208,6 +208,7 @@ __device__ __forceinline__ void helmholtz_sell_row(const EvalParams& a, int64_t 
           si[q] = fma(hci, g1, hmi * t0);
         }
       } else {
+      double pm[NT], pc[NT];
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
         cg[q] = fma(dz, tz[q], fma(dy, ty[q], dx * tx[q])) * iR;

@@ -179,6 +179,11 @@ constexpr unsigned kWalkAbove = TSQBX_WALK_ABOVE;
 #define TSQBX_INT4_STORES 1
 #endif
 constexpr bool kInt4Stores = TSQBX_INT4_STORES != 0;
+// locate and L1-prefetch the next tile's candidates before testing this one
+#ifndef TSQBX_SWEEP_PREFETCH
+#define TSQBX_SWEEP_PREFETCH 1
+#endif
+constexpr bool kSweepPrefetch = TSQBX_SWEEP_PREFETCH != 0;
 
 // MODE 0: count members per row; 1: fill the SELL column (plus the row length
 // when `cnt` is given); 3: fill the CSR row; 2: bound -- no distance tests, the
@@ -297,20 +302,32 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
     for (int q = 0; q < kMaxCells / 32; ++q) sm.cell_en[lane + 32 * q] = pre[q];
     __syncwarp();
     const int nc = min(ncell, kMaxCells);
+    // sorted-source index of candidate t: the last cell with prefix <= t
+    auto cand = [&](int t) {
+      int lo_c = 0, hi_c = nc - 1;
+      while (lo_c < hi_c) {
+        const int mid = (lo_c + hi_c + 1) >> 1;
+        if (sm.cell_en[mid] <= t) lo_c = mid;
+        else hi_c = mid - 1;
+      }
+      return sm.cell_st[lo_c] + (t - sm.cell_en[lo_c]);
+    };
+    // the next tile's candidates are located and prefetched into L1 before the
+    // current tile is tested, so its staging gathers hit L1 instead of waiting
+    // on L2/HBM (TSQBX_SWEEP_PREFETCH)
+    int jn[kTile / 32];
+#pragma unroll
+    for (int r = 0; r < kTile / 32; ++r) jn[r] = lane + 32 * r < min(kTile, total) ? cand(lane + 32 * r) : 0;
     for (int base = 0; base < total; base += kTile) {
       const int fill = min(kTile, total - base);
+      int jc[kTile / 32];
+#pragma unroll
+      for (int r = 0; r < kTile / 32; ++r) jc[r] = jn[r];
 #pragma unroll
       for (int r = 0; r < kTile / 32; ++r) {
         const int q = lane + 32 * r;
         if (q < fill) {
-          const int t = base + q;
-          int lo_c = 0, hi_c = nc - 1;               // last cell with prefix <= t
-          while (lo_c < hi_c) {
-            const int mid = (lo_c + hi_c + 1) >> 1;
-            if (sm.cell_en[mid] <= t) lo_c = mid;
-            else hi_c = mid - 1;
-          }
-          const int j = sm.cell_st[lo_c] + (t - sm.cell_en[lo_c]);
+          const int j = jc[r];
           const double4 sj = sxyz[j];
           const float x = (float)(sj.x - ox), y = (float)(sj.y - oy), z = (float)(sj.z - oz);
           float* pa = reinterpret_cast<float*>(&sm.tab[q >> 1]) + (q & 1);
@@ -323,6 +340,21 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
         }
       }
       __syncwarp();
+      if (kSweepPrefetch && base + kTile < total) {
+        const int nb = base + kTile, nfill = min(kTile, total - nb);
+#pragma unroll
+        for (int r = 0; r < kTile / 32; ++r) {
+          const int q = lane + 32 * r;
+          if (q < nfill) {
+            jn[r] = cand(nb + q);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(sxyz + jn[r]));
+          }
+        }
+      } else if (!kSweepPrefetch && base + kTile < total) {
+#pragma unroll
+        for (int r = 0; r < kTile / 32; ++r)
+          if (lane + 32 * r < min(kTile, total - base - kTile)) jn[r] = cand(base + kTile + lane + 32 * r);
+      }
       if (mine) {
         // test 32 staged candidates into a per-lane bit mask, then append only
         // this lane's members (no per-candidate divergent work in the fill)
