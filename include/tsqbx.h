@@ -72,6 +72,10 @@ extern "C" {
  * (a warp's 32 rows' entries split evenly over its lanes) instead of the
  * SELL thread-per-row kernel -- for near lists of a few dozen sources. */
 #define TSQBX_FLAG_FLAT (1u << 17)
+/* Laplace S on the SELL layout with uniform target runs and unsplit rows:
+ * two rows per thread, the second row's loads in flight while the first
+ * computes (short near lists: fewer waves of dependent-load chains). */
+#define TSQBX_FLAG_TWO_ROWS (1u << 18)
 
 #define TSQBX_MAX_ORDER 64
 

@@ -39,6 +39,7 @@ FLAG_KR_NARROW = 64
 FLAG_KR_WIDE = 128
 FLAG_LONG_ROWS = 1 << 16
 FLAG_FLAT = 1 << 17
+FLAG_TWO_ROWS = 1 << 18
 MAX_ORDER = 64
 ERR_KEY_NONE = (1 << 63) - 1
 ERR_KEY_SUSPECT = (1 << 63) - 2

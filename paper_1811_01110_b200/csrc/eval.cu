@@ -624,6 +624,7 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
   a.series = (flags & TSQBX_FLAG_KR_NARROW) ? 1 : (flags & TSQBX_FLAG_KR_WIDE) ? 2 : 0;
 #endif
   a.long_rows = (flags & TSQBX_FLAG_LONG_ROWS) ? 1 : 0;
+  a.two_rows = (flags & TSQBX_FLAG_TWO_ROWS) ? 1 : 0;
   if (equation == TSQBX_EQ_HELMHOLTZ) {
     a.ttab_stride = fast ? p + 1 : 2 * (p + 1);
     const int64_t need = n_tgt * a.ttab_stride * (int64_t)sizeof(double);

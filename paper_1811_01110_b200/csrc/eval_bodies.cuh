@@ -16,7 +16,8 @@ namespace tsqbx {
 template <int P, int NT, bool VAL, bool REALW, int S = 1>
 __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g,
                                                   const RowHead& h, int4* ring, int part = 0,
-                                                  unsigned gmask = 0xffffffffu) {
+                                                  unsigned gmask = 0xffffffffu,
+                                                  bool issued = false, bool foreign = false) {
   const double cx = h.cx, cy = h.cy, cz = h.cz;
   const int len = h.len;
   const int64_t t0 = h.t0, t1 = h.t1;
@@ -25,7 +26,7 @@ __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g
   // the dense presets) keep one in flight (C4 dense +2.2 %)
   using Stream = SellStream<false, (P >= 12 && S == 1 ? 2 : TSQBX_GATHER_DEPTH)>;
   // the index ring starts filling before the target range is known
-  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S);
+  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S, issued, foreign);
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];
     // VAL: min |s-c|^2 over the row as its IEEE bit pattern (R^2 >= 0, so the

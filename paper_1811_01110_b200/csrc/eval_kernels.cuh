@@ -40,6 +40,7 @@ struct EvalParams {
   SincCosCoeffs sc;                  // sin/cos series (kSincCos), constant-bank operands
   int series;                        // 0: per-warp vote; 1: narrow only; 2: wide (library past pi/2)
   int long_rows;                     // TSQBX_FLAG_LONG_ROWS: kernels tuned for long near lists
+  int two_rows;                      // TSQBX_FLAG_TWO_ROWS: Laplace S, two rows per thread
 };
 
 int64_t packed_doubles(int64_t n, int with_normals);
@@ -194,9 +195,14 @@ struct SellStream {
   // first kRing index blocks (start() later waits for block 0 and gathers).
   // b0 / bs: this thread takes the row's blocks b0, b0 + bs, ... (a row split
   // over bs threads); `count` becomes the number of entries in those blocks.
+  // issued: the first kRing blocks were already issued (by an earlier
+  // SellStream over the same row and ring); foreign: kRing cp.async groups of
+  // another row were committed right after them (laplace_sell2_kernel), so
+  // waiting for one of the first kRing blocks leaves 2 kRing - 1 groups pending
+  bool foreign = false;
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t soff, int64_t g, int n,
                                         bool realw, int4* ring_base, bool go, int b0 = 0,
-                                        int bs = 1)
+                                        int bs = 1, bool issued = false, bool foreign_ = false)
       : sp(a.sp), swi(a.swi), count(n), i(0), real_w(realw), snrm(a.snrm) {
     const int nb = (n + 3) >> 2;                       // blocks of the whole row
     blk = reinterpret_cast<const int4*>(a.sell_idx + soff) + (g & 31) + 32 * b0;
@@ -204,7 +210,8 @@ struct SellStream {
     ring = ring_base + threadIdx.x;
     nblk = nb > b0 ? (nb - b0 + bs - 1) / bs : 0;
     count = nblk == 0 ? 0 : 4 * (nblk - 1) + min(4, n - 4 * (b0 + bs * (nblk - 1)));
-    issue_first();
+    foreign = foreign_;
+    if (!issued) issue_first();
     if (go) start();
   }
   __device__ __forceinline__ void issue_first() {
@@ -229,7 +236,8 @@ struct SellStream {
     start();
   }
   __device__ __forceinline__ void enter_block(int b) {
-    cp_async_wait<kRing - 1>();                 // block b has landed
+    if (foreign && b < kRing) cp_async_wait<2 * kRing - 1>();
+    else cp_async_wait<kRing - 1>();            // block b has landed
     cur = ring[(b % kSlots) * kSellBlock];
     issue(b + kRing);                           // reuses the slot of block b - 1
   }

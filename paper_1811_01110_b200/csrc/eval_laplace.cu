@@ -137,6 +137,39 @@ __global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : (UNI >
   CTA_END();
 }
 
+// Two rows per thread (short near lists, uniform target runs): a warp takes two
+// adjacent slices, lane l rows 64 w + l (A) and 64 w + 32 + l (B) -- Morton
+// neighbours, so both rows gather from the same L1-resident sources.  Both rows' heads are loaded and
+// both index rings start filling before row A computes, so row B's dependent
+// chain (slice offset -> index block -> source record) is served while row A
+// evaluates instead of in a second wave of threads.
+#ifndef TSQBX_LAP_MINB2
+#define TSQBX_LAP_MINB2 3
+#endif
+template <int P, int NT, bool VAL, int UNI>
+__global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB2) laplace_sell2_kernel(const EvalParams a) {
+  __shared__ int4 ring[2][kSlots * kSellBlock];
+  const int64_t ga = ((int64_t)blockIdx.x * (kSellBlock / 32) + (threadIdx.x >> 5)) * 64 +
+                     (threadIdx.x & 31);
+  const int64_t gb = ga + 32;
+  if (ga >= a.n_ctr) return;
+  const bool has_b = gb < a.n_ctr;
+  const RowHead ha = load_head<UNI>(a, ga);
+  RowHead hb{};
+  if (has_b) hb = load_head<UNI>(a, gb);
+  const bool realw = a.real_w || *a.imag_flag == 0u;
+  using Stream = SellStream<false, (P >= 12 ? 2 : TSQBX_GATHER_DEPTH)>;
+  { Stream pre(a, ha.soff, ga, ha.len, realw, ring[0], false); }   // A's first blocks
+  if (has_b) { Stream pre(a, hb.soff, gb, hb.len, realw, ring[1], false); }   // then B's
+  if (realw) {
+    laplace_sell_body<P, NT, VAL, true, 1>(a, ga, ha, ring[0], 0, 0xffffffffu, true, has_b);
+    if (has_b) laplace_sell_body<P, NT, VAL, true, 1>(a, gb, hb, ring[1], 0, 0xffffffffu, true);
+  } else {
+    laplace_sell_body<P, NT, VAL, false, 1>(a, ga, ha, ring[0], 0, 0xffffffffu, true, has_b);
+    if (has_b) laplace_sell_body<P, NT, VAL, false, 1>(a, gb, hb, ring[1], 0, 0xffffffffu, true);
+  }
+}
+
 template <template <int> class F, int... Ps>
 struct OrderTable {
   template <class... Args>
@@ -160,6 +193,11 @@ struct LaplaceLaunch {
     if (sell) {
       // on the SELL layout `group_lanes` is the row split S (threads per row)
       const int S = (a.G == 2 || a.G == 4) ? a.G : 1;
+      if (S == 1 && a.two_rows && a.tuni == NT) {
+        const int blocks2 = (int)((n_ctr + 2 * kSellBlock - 1) / (2 * kSellBlock));
+        laplace_sell2_kernel<P, NT, VAL, NT><<<blocks2, kSellBlock, 0, st>>>(a);
+        return;
+      }
       const int rows = kSellBlock / S;
       const int blocks = (int)((n_ctr + rows - 1) / rows);
       if (a.tuni == NT) sell_launch<NT, VAL, NT>(S, blocks, a, st);

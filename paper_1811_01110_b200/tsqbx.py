@@ -96,6 +96,24 @@ def pick_flat(mean_len: float) -> bool:
     return mean_len < FLAT_BELOW
 
 
+# Mean near-list length below which Laplace S would take two rows per thread
+# (laplace_sell2_kernel).  0 = never: measured slower on the literal presets
+# (C2 literal 31.4 vs 27.1 us, C4 literal 58.2 vs 49.6 us): a thread's row-B
+# chain is hidden, but its entries' source gathers now queue behind row A's
+# -- the literal kernels wait on per-entry gathers, not on the row heads.
+TWO_ROWS_BELOW = 0.0
+
+
+def pick_two_rows(mean_len: float) -> bool:
+    """Short lists (the literal presets): laplace_sell2_kernel, two rows per
+    thread with the second row's loads in flight during the first row's
+    arithmetic.  GIGAQBX_TWO_ROWS=0/1 overrides."""
+    env = os.environ.get("GIGAQBX_TWO_ROWS")
+    if env is not None:
+        return env == "1"
+    return mean_len < TWO_ROWS_BELOW
+
+
 def pick_layout() -> str:
     """'sell' (thread per center on the sliced-ELL copy, the default) or 'csr'
     (groups of lanes per center on the CSR rows); GIGAQBX_LAYOUT overrides."""
@@ -190,6 +208,7 @@ class _Prepared:
         self.one_target = os.environ.get("GIGAQBX_ONE_TARGET", "0") == "1"
         self.tuni = 0         # k > 0: every row owns k consecutive targets (set_uniform_targets)
         self.flat = False     # Laplace S, uniform runs of 1-2 targets, short lists: flat kernel
+        self.two_rows = False  # Laplace S, uniform runs, unsplit rows: two rows per thread
         self._auto_split = (not group_lanes and self.layout == "sell" and spec.is_laplace
                             and self.variant == 0 and "GIGAQBX_SPLIT" not in os.environ)
         # Helmholtz: every near source lies within the largest near radius, so
@@ -214,6 +233,8 @@ class _Prepared:
             self.flat = (k <= 2 and self.layout == "sell" and self.cfg.spec.is_laplace
                          and self.variant == 0 and self.cfg.p_qbx <= 16
                          and pick_flat(self.near.mean_len))
+            self.two_rows = (k <= 2 and self.layout == "sell" and self.cfg.spec.is_laplace
+                             and self.variant == 0 and pick_two_rows(self.near.mean_len))
             if self._auto_split:          # the uniform kernel fits one more CTA per SM
                 self.G = pick_split(self.near.mean_len, self.n_ctr, k == 1,
                                     dv.sm_count(self.dev.index if self.dev.index is not None
@@ -263,6 +284,8 @@ class _Prepared:
         flat = self.flat and fast
         if flat:
             flags |= _lib.FLAG_FLAT
+        if self.two_rows and G == 1:
+            flags |= _lib.FLAG_TWO_ROWS
         csr = None if (sell and fast and not flat) else near.idx
         _lib.check(L.tsqbx_eval_packed(
             self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,
