@@ -166,6 +166,16 @@ constexpr int kSlots = kRing + 1;  // ring slots per thread (a power of two keep
 #ifndef TSQBX_GATHER_DEPTH
 #define TSQBX_GATHER_DEPTH 1
 #endif
+// SELL streams: L1-prefetch the next index block's source records on entering
+// a block (their gathers then hit L1).  Off: measured 2-6 % slower on every
+// preset (C2 literal 29.2 vs 27.3 us, C5 dense 12.94 vs 12.30 ms)
+#ifndef TSQBX_REC_PREFETCH
+#define TSQBX_REC_PREFETCH 0
+#endif
+constexpr bool kRecPrefetch = TSQBX_REC_PREFETCH != 0;
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 // D = source records gathered ahead of use (1: the next one; 2: two deep)
 template <bool NRM = false, int D = TSQBX_GATHER_DEPTH>
@@ -236,8 +246,24 @@ struct SellStream {
     start();
   }
   __device__ __forceinline__ void enter_block(int b) {
-    if (foreign && b < kRing) cp_async_wait<2 * kRing - 1>();
-    else cp_async_wait<kRing - 1>();            // block b has landed
+    if (foreign) {
+      if (b < kRing) cp_async_wait<2 * kRing - 1>();
+      else cp_async_wait<kRing - 1>();          // block b has landed
+    } else if (kRecPrefetch && kRing >= 2) {
+      // blocks b and b + 1 have landed: the source records of block b + 1 go
+      // into L1 now, 4-8 entries ahead of their gathers
+      cp_async_wait<kRing - 2>();
+      if (b + 1 < nblk) {
+        const int4 nx = ring[((b + 1) % kSlots) * kSellBlock];
+        const int e = 4 * (b + 1);
+        prefetch_l1(sp + nx.x);
+        if (e + 1 < count) prefetch_l1(sp + nx.y);
+        if (e + 2 < count) prefetch_l1(sp + nx.z);
+        if (e + 3 < count) prefetch_l1(sp + nx.w);
+      }
+    } else {
+      cp_async_wait<kRing - 1>();               // block b has landed
+    }
     cur = ring[(b % kSlots) * kSellBlock];
     issue(b + kRing);                           // reuses the slot of block b - 1
   }
