@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 10
+#define TSQBX_ABI_VERSION 11
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -76,6 +76,9 @@ extern "C" {
  * two rows per thread, the second row's loads in flight while the first
  * computes (short near lists: fewer waves of dependent-load chains). */
 #define TSQBX_FLAG_TWO_ROWS (1u << 18)
+/* Laplace S on a windowed SELL layout (tsqbx_sell_window; set by
+ * tsqbx_eval_packed_win, rejected by tsqbx_eval_packed). */
+#define TSQBX_FLAG_WINDOW (1u << 19)
 
 #define TSQBX_MAX_ORDER 64
 
@@ -286,6 +289,32 @@ int tsqbx_sell_size(int64_t n_rows, const int64_t* near_ptr, void* workspace, in
                     int64_t* sell_ptr, int64_t* n_entries, void* stream);
 int tsqbx_sell_fill(int64_t n_rows, const int64_t* near_ptr, const int32_t* near_idx,
                     const int64_t* sell_ptr, int32_t* sell_idx, void* stream);
+
+/* tsqbx_eval_packed on a windowed SELL layout (TSQBX_FLAG_WINDOW implied):
+ * sell_loc / win_src / win_len from tsqbx_sell_window, near_idx the plain CSR
+ * entries (validation only).  Laplace S, p <= 16, uniform target runs,
+ * group_lanes 1. */
+int tsqbx_eval_packed_win(int equation, int variant, double k, int p, const double* packed,
+                          int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
+                          const int64_t* near_ptr, const int32_t* near_idx,
+                          const int64_t* sell_ptr, const int32_t* sell_loc,
+                          const int32_t* win_src, const int32_t* win_len, const double* tgt_xyz,
+                          const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
+                          const int64_t* tgt_out, int64_t out_offset, int64_t tgt_base,
+                          unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
+                          double* out, int64_t* err_key, void* stream);
+/* Windowed SELL for short near lists: for every 32-row slice its distinct
+ * sources (at most TSQBX_WINDOW, win_src[s * TSQBX_WINDOW + i], count
+ * win_len[s]) and loc_idx = the SELL entries as indices into that window
+ * (same positions as sell_idx).  A slice with more distinct sources than
+ * TSQBX_WINDOW keeps its global indices in loc_idx, gets win_len = -1 and is
+ * counted in *overflow (device unsigned).  Evaluated with
+ * TSQBX_FLAG_WINDOW: a warp stages its slice's window in shared memory once
+ * and its rows read their sources from there. */
+#define TSQBX_WINDOW 128
+int tsqbx_sell_window(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,
+                      const int32_t* sell_idx, int32_t* loc_idx, int32_t* win_src,
+                      int32_t* win_len, unsigned* overflow, void* stream);
 
 /* CSR entries (near_idx, rows by near_ptr) from a SELL-32x4 copy. */
 /* Copy a SELL-32x4 layout into one with narrower slices (every slice of the

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
                                                                "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
-ABI_VERSION = 10      # TSQBX_ABI_VERSION in include/tsqbx.h
+ABI_VERSION = 11      # TSQBX_ABI_VERSION in include/tsqbx.h
 
 # status codes (include/tsqbx.h)
 OK = 0
@@ -40,6 +40,8 @@ FLAG_KR_WIDE = 128
 FLAG_LONG_ROWS = 1 << 16
 FLAG_FLAT = 1 << 17
 FLAG_TWO_ROWS = 1 << 18
+FLAG_WINDOW = 1 << 19
+WINDOW = 128
 MAX_ORDER = 64
 ERR_KEY_NONE = (1 << 63) - 1
 ERR_KEY_SUSPECT = (1 << 63) - 2
@@ -78,6 +80,10 @@ SIGNATURES = {
     "tsqbx_near_workspace_bytes": (_I64, [_I64, _I64]),
     "tsqbx_near_count": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "tsqbx_near_fill": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "tsqbx_eval_packed_win": (_I, [_I, _I, _D, _I, _P, _I64, _I, _P, _I64, _P, _P, _P, _P, _P, _P,
+                                   _P, _P, _P, _I64, _P, _I64, _I64, _U, _I, _P, _I64, _P, _P,
+                                   _P]),
+    "tsqbx_sell_window": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tsqbx_near_index": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P]),
     "tsqbx_fused_scratch_bytes": (_I64, [_I, _I, _I, _I, _I]),
     "tsqbx_eval_fused": (_I, [_I, _D, _I, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P, _I64, _P,

@@ -545,14 +545,15 @@ int64_t tsqbx_eval_workspace_bytes(int equation, int variant, int p, int64_t n_t
   return n_tgt * 2 * (p + 1) * (int64_t)sizeof(double) + 256;
 }
 
-int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* packed,
-                      int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
-                      const int64_t* near_ptr, const int32_t* near_idx,
-                      const int64_t* sell_ptr, const int32_t* sell_idx, const double* tgt_xyz,
-                      const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
-                      const int64_t* tgt_out, int64_t out_offset, int64_t tgt_base,
-                      unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
-                      double* out, int64_t* err_key, void* stream) {
+static int eval_packed_impl(int equation, int variant, double k, int p, const double* packed,
+                            int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
+                            const int64_t* near_ptr, const int32_t* near_idx,
+                            const int64_t* sell_ptr, const int32_t* sell_idx,
+                            const double* tgt_xyz, const double* tgt_nrm, const int64_t* tgt_ptr,
+                            int64_t n_tgt, const int64_t* tgt_out, int64_t out_offset,
+                            int64_t tgt_base, unsigned flags, int group_lanes, void* workspace,
+                            int64_t ws_bytes, double* out, int64_t* err_key, void* stream,
+                            const int32_t* win_src, const int32_t* win_len) {
   cudaStream_t st = (cudaStream_t)stream;
   if (equation != TSQBX_EQ_LAPLACE && equation != TSQBX_EQ_HELMHOLTZ)
     return set_error(TSQBX_ERR_ARGUMENT, "bad equation %d", equation);
@@ -625,6 +626,17 @@ int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* 
 #endif
   a.long_rows = (flags & TSQBX_FLAG_LONG_ROWS) ? 1 : 0;
   a.two_rows = (flags & TSQBX_FLAG_TWO_ROWS) ? 1 : 0;
+  // windowed SELL: Laplace S only (the sell_idx entries are window indices)
+  if (flags & TSQBX_FLAG_WINDOW) {
+    if (!win_src || !win_len || !sell_ptr || equation != TSQBX_EQ_LAPLACE || variant != 0 ||
+        p > kMaxFastOrder || (flags & TSQBX_FLAG_GENERIC) || !(flags & TSQBX_FLAG_UNIFORM_TARGETS) ||
+        group_lanes > 1)
+      return set_error(TSQBX_ERR_ARGUMENT,
+                       "window layout: Laplace S, p <= 16, uniform targets, unsplit rows, "
+                       "win_src / win_len / sell_ptr given");
+    a.win_src = win_src;
+    a.win_len = win_len;
+  }
   if (equation == TSQBX_EQ_HELMHOLTZ) {
     a.ttab_stride = fast ? p + 1 : 2 * (p + 1);
     const int64_t need = n_tgt * a.ttab_stride * (int64_t)sizeof(double);
@@ -663,6 +675,38 @@ int64_t tsqbx_user_workspace_bytes(int equation, int variant, int p, int64_t n_s
                                    int64_t n_tgt) {
   const int64_t packed = packed_doubles(n_src, variant == 2) * (int64_t)sizeof(double);
   return (packed + 255) / 256 * 256 + tsqbx_eval_workspace_bytes(equation, variant, p, n_tgt);
+}
+
+int tsqbx_eval_packed(int equation, int variant, double k, int p, const double* packed,
+                      int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
+                      const int64_t* near_ptr, const int32_t* near_idx,
+                      const int64_t* sell_ptr, const int32_t* sell_idx, const double* tgt_xyz,
+                      const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
+                      const int64_t* tgt_out, int64_t out_offset, int64_t tgt_base,
+                      unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
+                      double* out, int64_t* err_key, void* stream) {
+  if (flags & TSQBX_FLAG_WINDOW)
+    return set_error(TSQBX_ERR_ARGUMENT, "TSQBX_FLAG_WINDOW needs tsqbx_eval_packed_win");
+  return eval_packed_impl(equation, variant, k, p, packed, n_src, with_normals, ctr_xyz, n_ctr,
+                          near_ptr, near_idx, sell_ptr, sell_idx, tgt_xyz, tgt_nrm, tgt_ptr,
+                          n_tgt, tgt_out, out_offset, tgt_base, flags, group_lanes, workspace,
+                          ws_bytes, out, err_key, stream, nullptr, nullptr);
+}
+
+int tsqbx_eval_packed_win(int equation, int variant, double k, int p, const double* packed,
+                          int64_t n_src, int with_normals, const double* ctr_xyz, int64_t n_ctr,
+                          const int64_t* near_ptr, const int32_t* near_idx,
+                          const int64_t* sell_ptr, const int32_t* sell_loc,
+                          const int32_t* win_src, const int32_t* win_len, const double* tgt_xyz,
+                          const double* tgt_nrm, const int64_t* tgt_ptr, int64_t n_tgt,
+                          const int64_t* tgt_out, int64_t out_offset, int64_t tgt_base,
+                          unsigned flags, int group_lanes, void* workspace, int64_t ws_bytes,
+                          double* out, int64_t* err_key, void* stream) {
+  return eval_packed_impl(equation, variant, k, p, packed, n_src, with_normals, ctr_xyz, n_ctr,
+                          near_ptr, near_idx, sell_ptr, sell_loc, tgt_xyz, tgt_nrm, tgt_ptr,
+                          n_tgt, tgt_out, out_offset, tgt_base, flags | TSQBX_FLAG_WINDOW,
+                          group_lanes, workspace, ws_bytes, out, err_key, stream, win_src,
+                          win_len);
 }
 
 static int eval_user(int equation, int variant, double k, int p, const double* src_xyz,

@@ -13,20 +13,22 @@
 
 namespace tsqbx {
 
-template <int P, int NT, bool VAL, bool REALW, int S = 1>
+template <int P, int NT, bool VAL, bool REALW, int S = 1, bool WIN = false>
 __device__ __forceinline__ void laplace_sell_body(const EvalParams& a, int64_t g,
                                                   const RowHead& h, int4* ring, int part = 0,
                                                   unsigned gmask = 0xffffffffu,
-                                                  bool issued = false, bool foreign = false) {
+                                                  bool issued = false, bool foreign = false,
+                                                  const double4* win_q = nullptr,
+                                                  const double* win_w = nullptr) {
   const double cx = h.cx, cy = h.cy, cz = h.cz;
   const int len = h.len;
   const int64_t t0 = h.t0, t1 = h.t1;
   // high orders have more arithmetic per source to cover a second gather in
   // flight (measured: C4 literal p = 12 +7 %; p = 8 -2 %); split rows (S > 1,
   // the dense presets) keep one in flight (C4 dense +2.2 %)
-  using Stream = SellStream<false, (P >= 12 && S == 1 ? 2 : TSQBX_GATHER_DEPTH)>;
+  using Stream = SellStream<false, (P >= 12 && S == 1 && !WIN ? 2 : TSQBX_GATHER_DEPTH), WIN>;
   // the index ring starts filling before the target range is known
-  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S, issued, foreign);
+  Stream ss(a, h.soff, g, len, REALW, ring, false, part, S, issued, foreign, win_q, win_w);
   for (int64_t tb = t0; tb < t1; tb += NT) {
     double tx[NT], ty[NT], tz[NT], r2[NT], ar[NT], ai[NT];
     // VAL: min |s-c|^2 over the row as its IEEE bit pattern (R^2 >= 0, so the

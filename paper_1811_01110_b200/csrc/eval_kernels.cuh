@@ -41,6 +41,8 @@ struct EvalParams {
   int series;                        // 0: per-warp vote; 1: narrow only; 2: wide (library past pi/2)
   int long_rows;                     // TSQBX_FLAG_LONG_ROWS: kernels tuned for long near lists
   int two_rows;                      // TSQBX_FLAG_TWO_ROWS: Laplace S, two rows per thread
+  const int32_t* __restrict__ win_src;   // TSQBX_FLAG_WINDOW: per slice its distinct sources
+  const int32_t* __restrict__ win_len;
 };
 
 int64_t packed_doubles(int64_t n, int with_normals);
@@ -178,7 +180,10 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
 }
 
 // D = source records gathered ahead of use (1: the next one; 2: two deep)
-template <bool NRM = false, int D = TSQBX_GATHER_DEPTH>
+// WIN: the rows' sources were staged in a shared-memory window (windowed SELL,
+// tsqbx_sell_window): the entries are window indices and sp / swi point into
+// the window (shared-memory loads instead of global gathers)
+template <bool NRM = false, int D = TSQBX_GATHER_DEPTH, bool WIN = false>
 struct SellStream {
   const int4* __restrict__ blk;   // this lane's block 0; block b at blk + 32 b
   const double4* __restrict__ sp;
@@ -212,8 +217,11 @@ struct SellStream {
   bool foreign = false;
   __device__ __forceinline__ SellStream(const EvalParams& a, int64_t soff, int64_t g, int n,
                                         bool realw, int4* ring_base, bool go, int b0 = 0,
-                                        int bs = 1, bool issued = false, bool foreign_ = false)
-      : sp(a.sp), swi(a.swi), count(n), i(0), real_w(realw), snrm(a.snrm) {
+                                        int bs = 1, bool issued = false, bool foreign_ = false,
+                                        const double4* win_q = nullptr,
+                                        const double* win_w = nullptr)
+      : sp(WIN ? win_q : a.sp), swi(WIN ? win_w : a.swi), count(n), i(0), real_w(realw),
+        snrm(a.snrm) {
     const int nb = (n + 3) >> 2;                       // blocks of the whole row
     blk = reinterpret_cast<const int4*>(a.sell_idx + soff) + (g & 31) + 32 * b0;
     blk_stride = 32 * bs;
@@ -268,8 +276,17 @@ struct SellStream {
     issue(b + kRing);                           // reuses the slot of block b - 1
   }
   __device__ __forceinline__ void fetch(int d, int s) {
-    q_next[d] = ld256(sp + s);
-    if (!real_w) w_next[d] = __ldg(swi + s);
+    if (WIN) {
+      const unsigned at = (unsigned)__cvta_generic_to_shared(sp + s);
+      double4 v;
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(at));
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(at + 16));
+      q_next[d] = v;
+      if (!real_w) w_next[d] = swi[s];
+    } else {
+      q_next[d] = ld256(sp + s);
+      if (!real_w) w_next[d] = __ldg(swi + s);
+    }
     if (NRM) n_next[d] = ld256(snrm + s);
   }
   __device__ __forceinline__ bool more() const { return i < count; }

@@ -170,6 +170,56 @@ __global__ void __launch_bounds__(kSellBlock, TSQBX_LAP_MINB2) laplace_sell2_ker
   }
 }
 
+constexpr int kWinRecBytes = (kSellBlock / 32) * TSQBX_WINDOW * 32;
+constexpr int kWinSmemBytes = kWinRecBytes + (kSellBlock / 32) * TSQBX_WINDOW * 8;
+
+// Windowed SELL (short lists, tsqbx_sell_window): every warp is one slice; it
+// stages its slice's distinct sources (<= TSQBX_WINDOW records) in shared
+// memory once -- all loads independent, issued together -- while its rows'
+// index rings fill, and the rows then read their sources from the window
+// instead of one dependent global gather per entry.
+template <int P, int NT, bool VAL, int UNI>
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? TSQBX_LAP_MINB1 : TSQBX_LAP_MINB_UNI)
+    laplace_sellw_kernel(const EvalParams a) {
+  __shared__ int4 ring[kSlots * kSellBlock];
+  // dynamic: [8 warps][W] double4 records, then [8 warps][W] Im w
+  extern __shared__ __align__(16) unsigned char win_smem[];
+  double4* wq_all = reinterpret_cast<double4*>(win_smem);
+  double* wwi_all = reinterpret_cast<double*>(win_smem + kWinRecBytes);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double4* wq = wq_all + w * TSQBX_WINDOW;
+  double* wwi = wwi_all + w * TSQBX_WINDOW;
+  const int64_t g = (int64_t)blockIdx.x * kSellBlock + threadIdx.x;
+  const int64_t s = g >> 5;
+  if ((s << 5) >= a.n_ctr) return;                 // warp-uniform
+  const bool valid = g < a.n_ctr;
+  RowHead h{};
+  if (valid) h = load_head<UNI>(a, g);
+  const bool realw = a.real_w || *a.imag_flag == 0u;
+  if (valid) {                                     // this row's first index blocks
+    SellStream<false, TSQBX_GATHER_DEPTH, true> pre(a, h.soff, g, h.len, realw, ring, false);
+  }
+  const int wl = a.win_len[s];
+  for (int i = lane; i < wl; i += 32) {
+    const int j = a.win_src[s * TSQBX_WINDOW + i];
+    wq[i] = ld256(a.sp + j);
+    if (!realw) wwi[i] = __ldg(a.swi + j);
+  }
+  __syncwarp();
+  if (!valid) return;
+  if (wl < 0) {            // an overflowed slice: global indices, global gathers
+    if (realw) laplace_sell_body<P, NT, VAL, true, 1>(a, g, h, ring, 0, 0xffffffffu, true);
+    else laplace_sell_body<P, NT, VAL, false, 1>(a, g, h, ring, 0, 0xffffffffu, true);
+    return;
+  }
+  if (realw)
+    laplace_sell_body<P, NT, VAL, true, 1, true>(a, g, h, ring, 0, 0xffffffffu, true, false,
+                                                 wq, wwi);
+  else
+    laplace_sell_body<P, NT, VAL, false, 1, true>(a, g, h, ring, 0, 0xffffffffu, true, false,
+                                                  wq, wwi);
+}
+
 template <template <int> class F, int... Ps>
 struct OrderTable {
   template <class... Args>
@@ -193,6 +243,17 @@ struct LaplaceLaunch {
     if (sell) {
       // on the SELL layout `group_lanes` is the row split S (threads per row)
       const int S = (a.G == 2 || a.G == 4) ? a.G : 1;
+      if (S == 1 && a.win_src && a.tuni == NT) {
+        static bool attr = false;   // once per instance: the window exceeds 48 KB of static smem
+        if (!attr) {
+          cudaFuncSetAttribute(laplace_sellw_kernel<P, NT, VAL, NT>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, kWinSmemBytes);
+          attr = true;
+        }
+        laplace_sellw_kernel<P, NT, VAL, NT><<<(int)((n_ctr + kSellBlock - 1) / kSellBlock),
+                                               kSellBlock, kWinSmemBytes, st>>>(a);
+        return;
+      }
       if (S == 1 && a.two_rows && a.tuni == NT) {
         const int blocks2 = (int)((n_ctr + 2 * kSellBlock - 1) / (2 * kSellBlock));
         laplace_sell2_kernel<P, NT, VAL, NT><<<blocks2, kSellBlock, 0, st>>>(a);

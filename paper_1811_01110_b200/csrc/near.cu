@@ -234,6 +234,88 @@ __global__ void sell_compact_kernel(int64_t n_sl, const int64_t* __restrict__ sp
   for (int64_t q = lane; q < n4; q += 32) dst[q] = src[q];
 }
 
+// Windowed SELL (short near lists): per 32-row slice, the unique sources of its
+// rows (at most TSQBX_WINDOW, in win_src[s * W ...], count win_len[s]) and the
+// entries rewritten as indices into that window (loc_idx, same SELL-32x4
+// positions as sell_idx).  A warp per slice: its lanes insert their rows'
+// entries into a shared-memory hash set (open addressing, 2W slots), rank the
+// occupied slots by a ballot scan, write the window and map every entry to its
+// rank.  A slice with more than W distinct sources keeps its global indices
+// (win_len = -1) and counts in *overflow.
+constexpr int kWinHash = 2 * TSQBX_WINDOW;
+__global__ void __launch_bounds__(128) sell_window_kernel(
+    const int64_t* __restrict__ nptr, int64_t n_rows, const int64_t* __restrict__ sptr,
+    const int32_t* __restrict__ sidx, int32_t* __restrict__ loc, int32_t* __restrict__ win_src,
+    int32_t* __restrict__ win_len, unsigned* __restrict__ overflow) {
+  __shared__ int32_t key[4][kWinHash];
+  __shared__ int16_t rank[4][kWinHash];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = g >> 5;
+  if ((s << 5) >= n_rows) return;                  // whole warps only
+  for (int i = lane; i < kWinHash; i += 32) key[w][i] = -1;
+  __syncwarp();
+  const int len = g < n_rows ? (int)(nptr[g + 1] - nptr[g]) : 0;
+  const int32_t* col = sidx + sptr[s] + 4 * (g & 31);
+  auto slot_of = [&](int32_t j, bool insert) {
+    unsigned h = ((unsigned)j * 2654435761u) % (unsigned)kWinHash;
+    for (int probe = 0; probe < kWinHash; ++probe) {
+      const int32_t cur = insert ? atomicCAS(&key[w][h], -1, j) : key[w][h];
+      if (cur == -1 || cur == j) return (int)h;
+      h = h + 1 == (unsigned)kWinHash ? 0u : h + 1;
+    }
+    return -1;
+  };
+  bool full = false;
+  for (int k = 0; k < len; ++k) full |= slot_of(col[((k >> 2) << 7) | (k & 3)], true) < 0;
+  __syncwarp();
+  // rank the occupied slots (slot order), lane l owning slots [l*R, l*R + R)
+  constexpr int R = kWinHash / 32;
+  int occ = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) occ += key[w][lane * R + i] != -1;
+  int pre = occ;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, off);
+    if (lane >= off) pre += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, pre, 31);
+  pre -= occ;
+  const bool over = __any_sync(0xffffffffu, full) || total > TSQBX_WINDOW;
+  if (over) {
+    // too many distinct sources for the window: this slice keeps global
+    // indices (win_len = -1; its warp gathers from HBM/L2 as the plain kernel)
+    if (lane == 0) {
+      win_len[s] = -1;
+      atomicAdd(overflow, 1u);
+    }
+    int32_t* lcol = loc + sptr[s] + 4 * (g & 31);
+    for (int k = 0; k < len; ++k) {
+      const int at = ((k >> 2) << 7) | (k & 3);
+      lcol[at] = col[at];
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int h = lane * R + i;
+    const int32_t j = key[w][h];
+    if (j != -1) {
+      rank[w][h] = (int16_t)pre;
+      win_src[s * TSQBX_WINDOW + pre] = j;
+      ++pre;
+    }
+  }
+  if (lane == 0) win_len[s] = total;
+  __syncwarp();
+  int32_t* lcol = loc + sptr[s] + 4 * (g & 31);
+  for (int k = 0; k < len; ++k) {
+    const int at = ((k >> 2) << 7) | (k & 3);
+    lcol[at] = rank[w][slot_of(col[at], false)];
+  }
+}
+
 __global__ void set_tail(int64_t* cnt, int64_t n) { cnt[n] = 0; }
 __global__ void set_key64(int64_t* p, int64_t v) { *p = v; }
 
@@ -659,6 +741,22 @@ int tsqbx_sell_compact(int64_t n_rows, const int64_t* sell_ptr_src, const int32_
   sell_compact_kernel<<<(unsigned)((n_sl * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       n_sl, sell_ptr_src, sell_idx_src, sell_ptr_dst, sell_idx_dst);
   return check_cuda(cudaGetLastError(), "sell_compact launch");
+}
+
+int tsqbx_sell_window(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,
+                      const int32_t* sell_idx, int32_t* loc_idx, int32_t* win_src,
+                      int32_t* win_len, unsigned* overflow, void* stream) {
+  if (n_rows < 0 || (n_rows > 0 && (!near_ptr || !sell_ptr || !sell_idx || !loc_idx ||
+                                    !win_src || !win_len || !overflow)))
+    return set_error(TSQBX_ERR_ARGUMENT, "sell_window: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(overflow, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return check_cuda(e, "sell_window memset");
+  if (n_rows == 0) return TSQBX_OK;
+  const int64_t threads = (n_rows + 31) / 32 * 32;
+  sell_window_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(
+      near_ptr, n_rows, sell_ptr, sell_idx, loc_idx, win_src, win_len, overflow);
+  return check_cuda(cudaGetLastError(), "sell_window launch");
 }
 
 int tsqbx_sell_to_csr(int64_t n_rows, const int64_t* near_ptr, const int64_t* sell_ptr,

@@ -47,6 +47,10 @@ class NearLists:
     sell_ptr: torch.Tensor | None = None
     sell_idx: torch.Tensor | None = None
     max_radius: float | None = None      # every entry has |s - c| <= max_radius (None: unknown)
+    # windowed SELL (short lists, build_window): window-local entries + windows
+    sell_loc: torch.Tensor | None = None
+    win_src: torch.Tensor | None = None
+    win_len: torch.Tensor | None = None
 
     @property
     def dev(self) -> torch.device:
@@ -93,6 +97,31 @@ class NearLists:
                                      sptr.data_ptr(), sidx.data_ptr(), st), "tsqbx_sell_fill")
         self.sell_ptr, self.sell_idx = sptr, sidx
         return self
+
+    @dv.on_own_device
+    def build_window(self) -> bool:
+        """The windowed SELL copy for short lists (``tsqbx_sell_window``): per
+        32-row slice its distinct sources (<= _lib.WINDOW) and the entries as
+        indices into them; a slice with more distinct sources than the window
+        keeps global indices (counted in ``win_overflow``)."""
+        if self.win_src is not None:
+            return True
+        if self.sell_ptr is None:
+            return False
+        L = _lib.load()
+        dev = self.ptr.device
+        n_sl = (self.n_ctr + 31) // 32
+        loc = torch.empty_like(self.sell_idx)
+        win = torch.empty(max(n_sl * _lib.WINDOW, 1), dtype=torch.int32, device=dev)
+        wlen = torch.zeros(max(n_sl, 1), dtype=torch.int32, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(L.tsqbx_sell_window(self.n_ctr, self.ptr.data_ptr(), self.sell_ptr.data_ptr(),
+                                       self.sell_idx.data_ptr(), loc.data_ptr(), win.data_ptr(),
+                                       wlen.data_ptr(), flag.data_ptr(), dv.stream_handle(dev)),
+                   "tsqbx_sell_window")
+        self.win_overflow = int(flag.item())      # slices that keep global indices
+        self.sell_loc, self.win_src, self.win_len = loc, win, wlen
+        return True
 
     @property
     def sell_fill(self) -> float:

@@ -103,6 +103,23 @@ def pick_flat(mean_len: float) -> bool:
 # -- the literal kernels wait on per-entry gathers, not on the row heads.
 TWO_ROWS_BELOW = 0.0
 
+# Mean near-list length below which Laplace S would use the windowed SELL.
+# 0 = never: measured slower on the literal presets (C2 literal 37.8 vs
+# 27.4 us, C4 literal 76 vs 50 us): the 40 KB window per CTA costs a quarter
+# of the resident warps and the staging adds a dependent step per warp, while
+# the per-entry gathers it removes were mostly L1 hits already.
+WINDOW_BELOW = 0.0
+
+
+def pick_window(mean_len: float) -> bool:
+    """Short lists: every warp stages its 32 rows' distinct sources in shared
+    memory once (tsqbx_sell_window + laplace_sellw_kernel) instead of one
+    global gather per entry.  GIGAQBX_WINDOW=0/1 overrides."""
+    env = os.environ.get("GIGAQBX_WINDOW")
+    if env is not None:
+        return env == "1"
+    return mean_len < WINDOW_BELOW
+
 
 def pick_two_rows(mean_len: float) -> bool:
     """Short lists (the literal presets): laplace_sell2_kernel, two rows per
@@ -209,6 +226,7 @@ class _Prepared:
         self.tuni = 0         # k > 0: every row owns k consecutive targets (set_uniform_targets)
         self.flat = False     # Laplace S, uniform runs of 1-2 targets, short lists: flat kernel
         self.two_rows = False  # Laplace S, uniform runs, unsplit rows: two rows per thread
+        self.window = False    # Laplace S, uniform runs, unsplit short rows: windowed SELL
         self._auto_split = (not group_lanes and self.layout == "sell" and spec.is_laplace
                             and self.variant == 0 and "GIGAQBX_SPLIT" not in os.environ)
         # Helmholtz: every near source lies within the largest near radius, so
@@ -240,6 +258,9 @@ class _Prepared:
                                     dv.sm_count(self.dev.index if self.dev.index is not None
                                                 else torch.cuda.current_device()),
                                     uniform=True)
+            self.window = (k <= 2 and self.layout == "sell" and self.cfg.spec.is_laplace
+                           and self.variant == 0 and self.cfg.p_qbx <= 16 and self.G == 1
+                           and pick_window(self.near.mean_len) and self.near.build_window())
 
     def pack(self, w: torch.Tensor) -> None:
         """(Re)pack the sources with weights ``w`` (interleaved float64 view)."""
@@ -287,6 +308,20 @@ class _Prepared:
         if self.two_rows and G == 1:
             flags |= _lib.FLAG_TWO_ROWS
         csr = None if (sell and fast and not flat) else near.idx
+        if (self.window and sell and fast and not flat and G == 1 and self.tuni
+                and near.win_src is not None):
+            _lib.check(L.tsqbx_eval_packed_win(
+                self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(),
+                self.n_src, self.with_normals, self.ctr.data_ptr() + 24 * g0, g1 - g0,
+                near.ptr.data_ptr() + 8 * g0, None,
+                near.sell_ptr.data_ptr() + 8 * (g0 // 32), near.sell_loc.data_ptr(),
+                near.win_src.data_ptr() + 4 * _lib.WINDOW * (g0 // 32),
+                near.win_len.data_ptr() + 4 * (g0 // 32), self.tgt.data_ptr(),
+                dv.ptr(self.tn), self.tptr.data_ptr() + 8 * g0, self.n_tgt,
+                dv.ptr(self.tidx) if user_order else None, out_offset, self.tuni * g0, flags, G,
+                self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.err.data_ptr(),
+                dv.stream_handle(self.dev)), "tsqbx_eval_packed_win")
+            return
         _lib.check(L.tsqbx_eval_packed(
             self.eq, self.variant, self.k, self.cfg.p_qbx, self.packed.data_ptr(), self.n_src,
             self.with_normals, self.ctr.data_ptr() + 24 * g0, g1 - g0,
