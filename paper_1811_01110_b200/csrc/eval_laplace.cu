@@ -244,12 +244,9 @@ struct LaplaceLaunch {
       // on the SELL layout `group_lanes` is the row split S (threads per row)
       const int S = (a.G == 2 || a.G == 4) ? a.G : 1;
       if (S == 1 && a.win_src && a.tuni == NT) {
-        static bool attr = false;   // once per instance: the window exceeds 48 KB of static smem
-        if (!attr) {
-          cudaFuncSetAttribute(laplace_sellw_kernel<P, NT, VAL, NT>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, kWinSmemBytes);
-          attr = true;
-        }
+        // the window exceeds the 48 KB default; per call (the attribute is per device)
+        cudaFuncSetAttribute(laplace_sellw_kernel<P, NT, VAL, NT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kWinSmemBytes);
         laplace_sellw_kernel<P, NT, VAL, NT><<<(int)((n_ctr + kSellBlock - 1) / kSellBlock),
                                                kSellBlock, kWinSmemBytes, st>>>(a);
         return;
