@@ -659,6 +659,17 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
                      user_tptr=tgt_ptr is not None)
     if tgt_ptr is None:
         prep.set_uniform_targets(known=True)
+    if _direct_out(out, prep):
+        # the kernel writes the potentials straight into the caller's pinned
+        # host buffer (mapped through unified addressing): the device-to-host
+        # copy overlaps the evaluation instead of following it
+        prep.launch(torch.view_as_real(out), validate)
+        if prep.n_tgt and validate:
+            prep.check_errors(batch_context=True)
+        else:
+            prep.check_inputs()
+        torch.cuda.current_stream(dev).synchronize()
+        return out
     res = torch.empty(prep.n_tgt, dtype=torch.complex128, device=dev)
     if prep.n_tgt:
         prep.launch(torch.view_as_real(res), validate)
@@ -667,6 +678,33 @@ def near_field_potentials(cfg: TsConfig, sources, weights, centers, near_radii, 
     else:
         prep.check_inputs()
     return _deliver(res, out, host_out)
+
+
+# Writing the potentials straight into pinned host memory moves the D2H copy
+# under the evaluation, but each scattered 16-byte store crosses PCIe: it pays
+# when the evaluation lasts longer than those stores take (~12 GB/s measured
+# for scattered complex128 stores): C5 dense 42.1 -> 39.6 ms end to end, C2
+# dense 2.18 -> 2.68 ms (a 0.3 ms kernel cannot hide 8 MB of stores).
+_DIRECT_OUT_GBS = 12.0
+_KERNEL_TFLOPS = 0.65 * 35.7       # the dense kernels' typical rate
+
+
+def _direct_out(out, prep) -> bool:
+    """Whether the kernels write into ``out`` (a pinned complex128 host tensor
+    of n_tgt entries) directly; GIGAQBX_DIRECT_OUT=0/1 overrides the estimate."""
+    n_tgt = prep.n_tgt
+    if not (isinstance(out, torch.Tensor) and out.device.type == "cpu" and out.is_pinned()
+            and out.dtype == torch.complex128 and out.is_contiguous()
+            and int(out.numel()) == n_tgt and n_tgt > 0):
+        return False
+    env = os.environ.get("GIGAQBX_DIRECT_OUT")
+    if env is not None:
+        return env == "1"
+    from .configs import algorithmic_flops_per_pair
+    pairs = prep.near.n_pairs * n_tgt / max(1, prep.n_ctr)
+    kernel_s = pairs * algorithmic_flops_per_pair(prep.cfg.spec, prep.cfg.p_qbx) / (
+        _KERNEL_TFLOPS * 1e12)
+    return kernel_s >= 16.0 * n_tgt / (_DIRECT_OUT_GBS * 1e9)
 
 
 class TsqbxProblem:

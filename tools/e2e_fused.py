@@ -22,7 +22,7 @@ for cs in sys.argv[1:] or ["c2/dense"]:
                                                    case.near_radii, case.targets, case.tgt_ptr))
     ho = torch.empty(case.n_targets, dtype=torch.complex128).pin_memory()
     res = {}
-    for fused in (True, False):
+    for fused in ((True, False) if os.environ.get("E2E_FUSED", "0") == "1" else (False,)):
         for _ in range(2):
             near_field_potentials(case.cfg, src, w, ctr, rad, tgt, tgt_ptr=tptr, out=ho,
                                   fused=fused)
@@ -35,7 +35,9 @@ for cs in sys.argv[1:] or ["c2/dense"]:
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
         res[fused] = (1e3 * float(np.median(ts)), ho.numpy().copy())
-    err = float(np.max(np.abs(res[True][1] - res[False][1])) / np.max(np.abs(res[False][1])))
-    pairs = None
-    print(f"{cs}: fused {res[True][0]:.3f} ms, two-step {res[False][0]:.3f} ms, "
-          f"speed-up {res[False][0] / res[True][0]:.2f}x, max rel diff {err:.1e}", flush=True)
+    if True in res:
+        err = float(np.max(np.abs(res[True][1] - res[False][1])) / np.max(np.abs(res[False][1])))
+        print(f"{cs}: fused {res[True][0]:.3f} ms, two-step {res[False][0]:.3f} ms, "
+              f"speed-up {res[False][0] / res[True][0]:.2f}x, max rel diff {err:.1e}", flush=True)
+    else:
+        print(f"{cs}: two-step {res[False][0]:.3f} ms", flush=True)
