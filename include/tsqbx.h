@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSQBX_ABI_VERSION 11
+#define TSQBX_ABI_VERSION 12
 
 #define TSQBX_OK 0
 #define TSQBX_ERR_SEPARATION 1   /* tsqbx.py:48-53  "separation violation for source i" */
@@ -223,6 +223,22 @@ int tsqbx_near_recount(const double* ctr_xyz, const double* radius, int64_t n_ct
                        int64_t n_src, void* workspace, int64_t ws_bytes,
                        const int32_t* ctr_order, int64_t* near_ptr, int64_t* totals,
                        void* stream);
+/* The exact route with the member masks kept between its two sweeps: the
+ * count writes one 32-bit word per (32-candidate group, center) into mask_ws
+ * (tsqbx_near_mask_bytes(n_ctr, totals[1] of the SELL-mode tsqbx_near_count)
+ * bytes, caller-owned), the SELL fill reads them back instead of staging and
+ * testing every candidate a second time.  Same results, same call order as
+ * tsqbx_near_recount / tsqbx_near_fill (sell_ptr from tsqbx_sell_size). */
+int64_t tsqbx_near_mask_bytes(int64_t n_ctr, int64_t n_sell_bound);
+int tsqbx_near_recount_masks(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                             int64_t n_src, void* workspace, int64_t ws_bytes,
+                             const int32_t* ctr_order, int64_t* near_ptr, int64_t* totals,
+                             void* mask_ws, int64_t mask_bytes, void* stream);
+int tsqbx_near_fill_masks(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                          int64_t n_src, void* workspace, int64_t ws_bytes,
+                          const int32_t* ctr_order, int64_t* near_ptr, const int64_t* sell_ptr,
+                          int32_t* sell_idx, int64_t* totals, const void* mask_ws,
+                          int64_t mask_bytes, void* stream);
 /* The bounding box, Morton sorts (src_perm, ctr_order) and cell hash of
  * tsqbx_near_count without any sweep: the state tsqbx_eval_fused reads. */
 int tsqbx_near_index(const double* ctr_xyz, const double* radius, int64_t n_ctr,

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("GIGAQBX_LIB_PATH") or os.path.join(HERE, "_lib",
                                                                "libgigaqbx_tsqbx.so")
 CSRC = os.path.join(HERE, "csrc")
 
-ABI_VERSION = 11      # TSQBX_ABI_VERSION in include/tsqbx.h
+ABI_VERSION = 12      # TSQBX_ABI_VERSION in include/tsqbx.h
 
 # status codes (include/tsqbx.h)
 OK = 0
@@ -89,6 +89,10 @@ SIGNATURES = {
     "tsqbx_eval_fused": (_I, [_I, _D, _I, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P, _I64, _P,
                               _U, _I, _P, _I64, _P, _P, _P]),
     "tsqbx_near_recount": (_I, [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
+    "tsqbx_near_mask_bytes": (_I64, [_I64, _I64]),
+    "tsqbx_near_recount_masks": (_I, [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P]),
+    "tsqbx_near_fill_masks": (_I, [_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
+                                   _P]),
     "tsqbx_near_fill_rows": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P,
                                   _P, _P]),
     "tsqbx_fp64_probe": (_I, [_P, _I64, _I, _I, _P]),

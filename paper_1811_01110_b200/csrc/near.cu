@@ -186,19 +186,23 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     const double4* __restrict__ sxyz, const unsigned long long* __restrict__ hkey,
     const int32_t* __restrict__ hst, const int32_t* __restrict__ hen, int64_t cap,
     int64_t* __restrict__ cnt, const int64_t* __restrict__ nptr, int32_t* __restrict__ nidx,
-    const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx) {
+    const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx,
+    const int64_t* __restrict__ mptr = nullptr, unsigned* __restrict__ mask = nullptr) {
   __shared__ SweepSmem sm[4];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = g < n_ctr;
-  // MODE 3: CSR row; MODE 1: SELL-32x4 column, entry k at dst[128 (k / 4) + k % 4]
+  // MODE 3: CSR row; MODE 1 / 5: SELL-32x4 column, entry k at dst[128 (k / 4) + k % 4]
   int32_t* dst = (MODE == 3 && valid) ? nidx + nptr[g]
-                 : (MODE == 1 && valid) ? sidx + sptr[g >> 5] + 4 * (g & 31) : nullptr;
+                 : ((MODE == 1 || MODE == 5) && valid) ? sidx + sptr[g >> 5] + 4 * (g & 31)
+                                                       : nullptr;
   const SweepIn in{ctr, rad, n_ctr, order, prm, sxyz, hkey, hst, hen, cap};
   int k = 0;
   int64_t ub = 0;
-  sweep_warp<MODE>(in, sm[threadIdx.x >> 5], g, dst, INT_MAX, k, ub);
-  if (MODE == 0 && valid) cnt[g] = k;
-  if (MODE == 1 && valid && cnt) cnt[g] = k;
+  // MODE 4 / 5: the slice's member masks (see near_sweep.cuh)
+  unsigned* mk = ((MODE == 4 || MODE == 5) && (g >> 5) * 32 < n_ctr) ? mask + mptr[g >> 5] : nullptr;
+  sweep_warp<MODE>(in, sm[threadIdx.x >> 5], g, dst, INT_MAX, k, ub, mk);
+  if ((MODE == 0 || MODE == 4) && valid) cnt[g] = k;
+  if ((MODE == 1 || MODE == 5) && valid && cnt) cnt[g] = k;
   if (MODE == 2 && (threadIdx.x & 31) == 0 && (g >> 5) * 32 < n_ctr)
     cnt[g >> 5] = 32 * ((ub + 3) & ~3ll);
 }
@@ -330,6 +334,15 @@ __global__ void sell_width(const int64_t* __restrict__ nptr, int64_t n_rows,
 }
 
 __global__ void sell_tail(int64_t* wid, int64_t n_sl) { wid[n_sl] = 0; }
+
+// mask words of a slice from its bound width (32 x its candidate bound, a
+// multiple of 4): 32 lanes x one word per 32-candidate group
+__global__ void mask_width(const int64_t* __restrict__ wid, int64_t n_sl,
+                           int64_t* __restrict__ mw) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > n_sl) return;
+  mw[s] = s < n_sl ? 32 * (((wid[s] >> 5) + 31) >> 5) : 0;
+}
 
 
 
@@ -614,6 +627,90 @@ int tsqbx_near_recount(const double* ctr_xyz, const double* radius, int64_t n_ct
                                         cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return check_cuda(e, "near_recount copy");
   return check_cuda(cudaGetLastError(), "near_recount launch");
+}
+
+int64_t tsqbx_near_mask_bytes(int64_t n_ctr, int64_t n_sell_bound) {
+  if (n_ctr < 0 || n_sell_bound < 0) return -1;
+  const int64_t n_sl = (n_ctr + 31) / 32;
+  // per slice 32 * ceil(bound / 32) words, bound = slice slots / 32
+  return (int64_t)(align256((n_sl + 1) * sizeof(int64_t)) +
+                   align256(sizeof(unsigned) * (size_t)(n_sell_bound / 32 + 32 * n_sl + 32)));
+}
+
+int tsqbx_near_recount_masks(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                             int64_t n_src, void* workspace, int64_t ws_bytes,
+                             const int32_t* ctr_order, int64_t* near_ptr, int64_t* totals,
+                             void* mask_ws, int64_t mask_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const NearLayout L = near_layout(n_ctr, n_src);
+  if (!workspace || ws_bytes < (int64_t)L.total)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_recount_masks: workspace too small");
+  const int64_t n_sl = (n_ctr + 31) / 32;
+  const size_t head = align256((n_sl + 1) * sizeof(int64_t));
+  if (!near_ptr || !totals || !mask_ws || mask_bytes < (int64_t)head ||
+      (n_ctr > 0 && (!ctr_xyz || !radius || !ctr_order)))
+    return set_error(TSQBX_ERR_ARGUMENT, "near_recount_masks: null array or mask workspace");
+  char* ws = static_cast<char*>(workspace);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
+  // mask offsets per slice from the bound widths the SELL-mode count left in
+  // the workspace (in-place scan)
+  int64_t* mptr = reinterpret_cast<int64_t*>(mask_ws);
+  unsigned* mask = reinterpret_cast<unsigned*>(static_cast<char*>(mask_ws) + head);
+  mask_width<<<(int)((n_sl + 256) / 256), 256, 0, st>>>(
+      reinterpret_cast<const int64_t*>(ws + L.off_wid), n_sl, mptr);
+  size_t tb = L.tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(ws + L.off_tmp, tb, mptr, mptr, (int)(n_sl + 1), st);
+  if (n_ctr > 0)
+    sweep_cell_kernel<4><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+        ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
+        reinterpret_cast<const double4*>(ws + L.off_sxyz),
+        reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
+        reinterpret_cast<const int32_t*>(ws + L.off_hst),
+        reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, cnt, nullptr, nullptr, nullptr,
+        nullptr, mptr, mask);
+  set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
+  tb = L.tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(ws + L.off_tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
+  const cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t),
+                                        cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "near_recount_masks copy");
+  return check_cuda(cudaGetLastError(), "near_recount_masks launch");
+}
+
+int tsqbx_near_fill_masks(const double* ctr_xyz, const double* radius, int64_t n_ctr,
+                          int64_t n_src, void* workspace, int64_t ws_bytes,
+                          const int32_t* ctr_order, int64_t* near_ptr, const int64_t* sell_ptr,
+                          int32_t* sell_idx, int64_t* totals, const void* mask_ws,
+                          int64_t mask_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const NearLayout L = near_layout(n_ctr, n_src);
+  if (!workspace || ws_bytes < (int64_t)L.total)
+    return set_error(TSQBX_ERR_ARGUMENT, "near_fill_masks: workspace too small");
+  const int64_t n_sl = (n_ctr + 31) / 32;
+  const size_t head = align256((n_sl + 1) * sizeof(int64_t));
+  if (!near_ptr || !totals || !sell_ptr || !sell_idx || !mask_ws || mask_bytes < (int64_t)head ||
+      (n_ctr > 0 && (!ctr_xyz || !radius || !ctr_order)))
+    return set_error(TSQBX_ERR_ARGUMENT, "near_fill_masks: null array or mask workspace");
+  char* ws = static_cast<char*>(workspace);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + L.off_cnt);
+  const int64_t* mptr = reinterpret_cast<const int64_t*>(mask_ws);
+  unsigned* mask = reinterpret_cast<unsigned*>(
+      const_cast<char*>(static_cast<const char*>(mask_ws)) + head);
+  if (n_ctr > 0)
+    sweep_cell_kernel<5><<<(int)((n_ctr + 127) / 128), 128, 0, st>>>(
+        ctr_xyz, radius, n_ctr, ctr_order, reinterpret_cast<const double*>(ws + L.off_prm),
+        reinterpret_cast<const double4*>(ws + L.off_sxyz),
+        reinterpret_cast<const unsigned long long*>(ws + L.off_hkey),
+        reinterpret_cast<const int32_t*>(ws + L.off_hst),
+        reinterpret_cast<const int32_t*>(ws + L.off_hen), L.cap, cnt, near_ptr, nullptr, sell_ptr,
+        sell_idx, mptr, mask);
+  set_tail<<<1, 1, 0, st>>>(cnt, n_ctr);
+  size_t tb = L.tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(ws + L.off_tmp, tb, cnt, near_ptr, (int)(n_ctr + 1), st);
+  const cudaError_t e = cudaMemcpyAsync(totals, near_ptr + n_ctr, sizeof(int64_t),
+                                        cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return check_cuda(e, "near_fill_masks copy");
+  return check_cuda(cudaGetLastError(), "near_fill_masks launch");
 }
 
 int tsqbx_near_fill_rows(const double* ctr_xyz, const double* radius, int64_t n_ctr,

@@ -189,6 +189,11 @@ constexpr bool kSweepPrefetch = TSQBX_SWEEP_PREFETCH != 0;
 // when `cnt` is given); 3: fill the CSR row; 2: bound -- no distance tests, the
 // slice width (32 x the largest candidate count of its rows, a multiple of 4)
 // into `cnt[slice]`, so the fill can write before the exact lengths are known.
+// MODE 4 / 5 (the exact route's count and SELL fill): as 0 / 1, but a warp in
+// union mode keeps its member masks -- the count writes one 32-bit word per
+// (32-candidate group, lane) to `mask` (word 32 * group + lane: a coalesced
+// 128-byte store per group), the fill reads them back instead of staging and
+// testing the candidates a second time.  Warps in per-cell mode test twice.
 struct SweepIn {
   const double* __restrict__ ctr;      // user order
   const double* __restrict__ rad;
@@ -220,7 +225,7 @@ struct SweepSmem {
 template <int MODE>
 __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int64_t g,
                                            int32_t* dst, int row_cap, int& k_out,
-                                           int64_t& ub_out) {
+                                           int64_t& ub_out, unsigned* mask = nullptr) {
   const double* __restrict__ ctr = in.ctr;
   const double* __restrict__ rad = in.rad;
   const int64_t n_ctr = in.n_ctr;
@@ -231,7 +236,8 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
   const int32_t* __restrict__ hst = in.hst;
   const int32_t* __restrict__ hen = in.hen;
   const int64_t cap = in.cap;
-  constexpr bool FILL = MODE == 1 || MODE == 3;
+  constexpr bool FILL = MODE == 1 || MODE == 3 || MODE == 5;
+  constexpr bool SELLF = MODE == 1 || MODE == 5;      // fill of a SELL column
   // staged candidates as fp32 offsets from the warp's reference point (see
   // run_cells) plus their sorted index; the exact fp64 test reads sxyz only for
   // the rare candidates inside the fp32 error band
@@ -258,14 +264,18 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
     ckey = morton3(ccx, ccy, ccz) | level_tag(lv);
   }
   int k = 0;
-  int4 pend = make_int4(0, 0, 0, 0);   // MODE 1 with kInt4Stores: the row's open block
+  int4 pend = make_int4(0, 0, 0, 0);   // SELL fill with kInt4Stores: the row's open block
   int64_t ub = 0;                      // MODE 2: candidates this row will test
   // Stage the sources of a list of up to kMaxCells cells (ranges [st, en) in
   // cell_st / cell_en of this warp, written by the caller) through the tile;
   // lanes with `mine` test them all.  o: the reference point (a center of this
   // warp); A: a bound on |p - o| (max norm) of every staged source and every
   // testing lane's center.
-  auto run_cells = [&](int ncell, bool mine, double ox, double oy, double oz, double A) {
+  // mk: the warp's member masks (MODE 4 writes them, MODE 5 reads them instead of
+  // staging coordinates and testing), nullptr = test here.
+  auto run_cells = [&](int ncell, bool mine, double ox, double oy, double oz, double A,
+                       unsigned* mk) {
+    const bool from_mask = MODE == 5 && mk != nullptr;
     // fp32 prefilter in dot-product form: with s' = s - o, c' = c - o (every
     // coordinate |.| <= A) a candidate is a member iff
     //   f = s'.c' - |s'|^2 / 2  >=  K = (|c'|^2 - rad^2) / 2,
@@ -326,7 +336,9 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
 #pragma unroll
       for (int r = 0; r < kTile / 32; ++r) {
         const int q = lane + 32 * r;
-        if (q < fill) {
+        if (q < fill && from_mask) {
+          sm.tid[q] = jc[r];
+        } else if (q < fill) {
           const int j = jc[r];
           const double4 sj = sxyz[j];
           const float x = (float)(sj.x - ox), y = (float)(sj.y - oy), z = (float)(sj.z - oz);
@@ -339,6 +351,11 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
           sm.tid[q] = j;
         }
       }
+      // MODE 5: this tile's mask words, all loads in flight before the appends
+      unsigned mw[kTile / 32];
+#pragma unroll
+      for (int r = 0; r < kTile / 32; ++r)
+        mw[r] = (from_mask && mine && 32 * r < fill) ? mk[(((base >> 5) + r) << 5) + lane] : 0u;
       __syncwarp();
       if (kSweepPrefetch && base + kTile < total) {
         const int nb = base + kTile, nfill = min(kTile, total - nb);
@@ -347,7 +364,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
           const int q = lane + 32 * r;
           if (q < nfill) {
             jn[r] = cand(nb + q);
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(sxyz + jn[r]));
+            if (!from_mask) asm volatile("prefetch.global.L1 [%0];" ::"l"(sxyz + jn[r]));
           }
         }
       } else if (!kSweepPrefetch && base + kTile < total) {
@@ -360,6 +377,13 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
         // this lane's members (no per-candidate divergent work in the fill)
         for (int t0 = 0; t0 < fill; t0 += 32) {
           const int m = min(32, fill - t0);
+          unsigned bits;
+          if (from_mask) {
+            bits = mw[0];
+#pragma unroll
+            for (int r = 1; r < kTile / 32; ++r)
+              if (t0 == 32 * r) bits = mw[r];
+          } else {
           // candidate u lands in bit 31 - u: each test shifts the sign bit of
           // f - K -/+ tau into a mask with one funnel shift (SHF); candidates
           // go in pairs through packed fp32 (FFMA2 / FADD2), so a pair costs
@@ -383,12 +407,14 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
           }
           // slots past `m` hold stale candidates (low bits): masked, not branched on
           const unsigned live = m == 32 ? ~0u : ~((1u << (32 - m)) - 1u);
-          unsigned bits = ~below_hi & live;                 // surely inside
+          bits = ~below_hi & live;                          // surely inside
           unsigned band = below_hi & ~below_lo & live;      // within tau of the sphere
           while (band) {                     // rare: the exact fp64 test
             const int u = __clz(band);
             band &= ~(0x80000000u >> u);
             if (member(sxyz[sm.tid[t0 + u]], cx, cy, cz, rad2)) bits |= 0x80000000u >> u;
+          }
+          if (MODE == 4 && mk) mk[((base + t0) & ~31) + lane] = bits;
           }
           if (!FILL) {
             k += __popc(bits);
@@ -400,7 +426,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
             // (every lane stores its own) beats a per-lane loop that runs as
             // long as the busiest lane
             auto put = [&](int j) {
-              if (MODE == 3 || !kInt4Stores) {
+              if (!SELLF || !kInt4Stores) {
                 if (k < row_cap) dst[MODE == 3 ? k : ((k >> 2) << 7) | (k & 3)] = j;
               } else {
                 // SELL: the row's current block as a 4-entry shift register,
@@ -527,7 +553,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
                    oz = __shfl_sync(0xffffffffu, cz, l0);
       const double cs = prm[3] * (double)(1ull << (kSubBits + lw));
       const double A = fmax(bhi[0] - blo[0], fmax(bhi[1] - blo[1], bhi[2] - blo[2])) + rb + 2.0 * cs;
-      run_cells(n_ne, valid, ox, oy, oz, A);
+      run_cells(n_ne, valid, ox, oy, oz, A, mask);
     }
   } else if (any_valid) {
     // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
@@ -562,11 +588,11 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
           sm.cell_en[lane] = en;
         }
         __syncwarp();
-        run_cells(27, valid && ckey == cell, ox, oy, oz, A);
+        run_cells(27, valid && ckey == cell, ox, oy, oz, A, nullptr);
       }
     }
   }
-  if (MODE == 1 && kInt4Stores && valid && (k & 3) && k < row_cap) {   // the last, partial block
+  if (SELLF && kInt4Stores && valid && (k & 3) && k < row_cap) {   // the last, partial block
     const int r = k & 3;                                // entries pending in pend's tail
     int4 blk = pend;
     if (r == 1) blk.x = pend.w;

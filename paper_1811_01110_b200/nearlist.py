@@ -19,6 +19,7 @@ A user-supplied CSR (user center rows, user source indices) is accepted too
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -181,6 +182,8 @@ def check_offsets(ptr: torch.Tensor, total: int, name: str) -> None:
 
 _BOUND_BYTES_MAX = 16 << 30     # bound-sized SELL buffer above this: count exactly
 _COMPACT_ABOVE = 1.5            # bound slots / exact slots above this: compact the slices
+# exact route: keep the count's member masks for the fill (GIGAQBX_EXACT_MASKS=0: test twice)
+_EXACT_MASKS = os.environ.get("GIGAQBX_EXACT_MASKS", "1") != "0"
 
 
 @dv.on_device
@@ -221,14 +224,26 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
         # slots, the fill then produces the exact row lengths
         n_sell = int(totals[1].item())
         exact = n_sell * 4 > _BOUND_BYTES_MAX
+        mws = None
         if exact:
             # a loose bound (union candidates far above the members, e.g. C5)
             # would need too much memory: count exactly (reusing the sorts and
-            # the cell hash), size the slices from the exact lengths, fill them
-            _lib.check(L.tsqbx_near_recount(dv.ptr(ctr), dv.ptr(rad), n_ctr, n_src,
-                                            ws.data_ptr(), ws_bytes, ctr_order.data_ptr(),
-                                            nptr.data_ptr(), totals.data_ptr(), st),
-                       "tsqbx_near_recount")
+            # the cell hash), size the slices from the exact lengths, fill them.
+            # The count keeps its member masks (one bit per candidate and
+            # center, ~1/30 of the bound-sized buffer) so the fill does not
+            # test the candidates a second time.
+            if _EXACT_MASKS:
+                mbytes = int(L.tsqbx_near_mask_bytes(n_ctr, n_sell))
+                mws = torch.empty(mbytes, dtype=torch.uint8, device=dev)
+                _lib.check(L.tsqbx_near_recount_masks(
+                    dv.ptr(ctr), dv.ptr(rad), n_ctr, n_src, ws.data_ptr(), ws_bytes,
+                    ctr_order.data_ptr(), nptr.data_ptr(), totals.data_ptr(), mws.data_ptr(),
+                    mbytes, st), "tsqbx_near_recount_masks")
+            else:
+                _lib.check(L.tsqbx_near_recount(dv.ptr(ctr), dv.ptr(rad), n_ctr, n_src,
+                                                ws.data_ptr(), ws_bytes, ctr_order.data_ptr(),
+                                                nptr.data_ptr(), totals.data_ptr(), st),
+                           "tsqbx_near_recount")
             wsb = int(L.tsqbx_sell_workspace_bytes(n_ctr))
             sws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
             _lib.check(L.tsqbx_sell_size(n_ctr, nptr.data_ptr(), sws.data_ptr(), wsb,
@@ -241,10 +256,16 @@ def build_near_lists(centers, sources, radii, device=None, sell: bool = True) ->
         n_pairs = int(totals[0].item())
         idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
         sidx = None
-    _lib.check(L.tsqbx_near_fill(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
-                                 ws.data_ptr(), ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
-                                 dv.ptr(idx), dv.ptr(sptr), dv.ptr(sidx), totals.data_ptr(), st),
-               "tsqbx_near_fill")
+    if sell and mws is not None:
+        _lib.check(L.tsqbx_near_fill_masks(dv.ptr(ctr), dv.ptr(rad), n_ctr, n_src, ws.data_ptr(),
+                                           ws_bytes, ctr_order.data_ptr(), nptr.data_ptr(),
+                                           sptr.data_ptr(), sidx.data_ptr(), totals.data_ptr(),
+                                           mws.data_ptr(), mbytes, st), "tsqbx_near_fill_masks")
+    else:
+        _lib.check(L.tsqbx_near_fill(dv.ptr(ctr), dv.ptr(rad), n_ctr, dv.ptr(src), n_src,
+                                     ws.data_ptr(), ws_bytes, ctr_order.data_ptr(),
+                                     nptr.data_ptr(), dv.ptr(idx), dv.ptr(sptr), dv.ptr(sidx),
+                                     totals.data_ptr(), st), "tsqbx_near_fill")
     if sell and exact:
         n_pairs = int(totals[0].item())
     elif sell:

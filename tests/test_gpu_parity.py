@@ -182,18 +182,20 @@ def _assert_sell_holds_csr(near, stride=1):
         assert np.array_equal(si[cells], d[p[g]:p[g + 1]])
 
 
-@pytest.mark.parametrize("mode", ["bound", "exact", "csr"])
+@pytest.mark.parametrize("mode", ["bound", "exact", "exact_nomask", "csr"])
 def test_near_list_build_paths_agree(mode, monkeypatch):
     """The bound-sized SELL build (+ compaction), the exact-count fallback it
     takes when the bound would be too large, and the CSR-only build give the
     same rows, the same SELL layout, and the oracle's membership."""
     from paper_1811_01110_b200 import nearlist
     case = configs.make_case("c5", "literal", n=32768, spheres=4)
-    if mode == "exact":
+    if mode.startswith("exact"):
         monkeypatch.setattr(nearlist, "_BOUND_BYTES_MAX", 0)
+        monkeypatch.setattr(nearlist, "_EXACT_MASKS", mode == "exact")
     near = build_near_lists(case.centers, case.sources, case.near_radii, sell=mode != "csr")
     if mode == "csr":
         near.build_sell()
+    monkeypatch.undo()
     ref = build_near_lists(case.centers, case.sources, case.near_radii)
     assert torch.equal(near.ptr, ref.ptr)
     assert torch.equal(near.idx, ref.idx)
@@ -205,6 +207,48 @@ def test_near_list_build_paths_agree(mode, monkeypatch):
     assert np.array_equal(uptr, optr)
     srt = np.concatenate([np.sort(uidx[uptr[i]:uptr[i + 1]]) for i in range(case.n_centers)])
     assert np.array_equal(srt, oidx)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["c2_dense", "c4_dense", "mixed", "sparse", "ragged"])
+def test_near_lists_exact_route_masks(kind, monkeypatch):
+    """The exact route with the count's member masks reused by the fill
+    (tsqbx_near_recount_masks / tsqbx_near_fill_masks): dense lists (union
+    mode, the uniform walk over 32-candidate groups), radii of mixed levels and
+    sparse centers (per-cell mode, which tests twice), a center count that is
+    not a multiple of 32 -- rows, SELL layout and oracle membership."""
+    from paper_1811_01110_b200 import nearlist
+    rng = np.random.default_rng(11)
+    if kind in ("c2_dense", "c4_dense"):
+        case = configs.make_case(kind[:2], "dense", n=16384)
+        ctr, src, rad = case.centers, case.sources, case.near_radii
+    elif kind == "mixed":
+        n = 30000
+        src = np.vstack([rng.normal(scale=0.05, size=(n // 2, 3)), rng.uniform(-1, 1, (n // 2, 3))])
+        ctr = src[rng.permutation(n)[: n // 2]] + rng.normal(scale=1e-3, size=(n // 2, 3))
+        rad = 0.004 * np.exp(rng.uniform(0.0, np.log(7.0), size=n // 2))
+    elif kind == "sparse":
+        src = rng.uniform(0, 1, (20000, 3))
+        ctr = rng.uniform(0, 1, (300, 3))
+        rad = np.full(300, 0.03)
+    else:
+        src = rng.normal(size=(3000, 3))
+        ctr = rng.normal(size=(1001, 3))
+        rad = rng.uniform(0.0, 0.6, size=1001)
+    monkeypatch.setattr(nearlist, "_BOUND_BYTES_MAX", 0)
+    monkeypatch.setattr(nearlist, "_EXACT_MASKS", True)
+    near = build_near_lists(ctr, src, rad)
+    monkeypatch.setattr(nearlist, "_EXACT_MASKS", False)
+    twice = build_near_lists(ctr, src, rad)
+    assert torch.equal(near.ptr, twice.ptr)
+    assert torch.equal(near.sell_ptr, twice.sell_ptr)
+    assert torch.equal(near.idx, twice.idx)
+    _assert_sell_holds_csr(near, stride=7)
+    uptr, uidx = near.to_user_csr()
+    optr, oidx = oracle.near_csr(ctr, rad, src)
+    assert np.array_equal(uptr, optr)
+    order = np.lexsort((uidx, np.repeat(np.arange(np.asarray(ctr).shape[0]), np.diff(uptr))))
+    assert np.array_equal(uidx[order], oidx)
 
 
 def test_near_lists_repeated_builds_are_exact():
