@@ -189,6 +189,8 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
     const int64_t* __restrict__ sptr, int32_t* __restrict__ sidx,
     const int64_t* __restrict__ mptr = nullptr, unsigned* __restrict__ mask = nullptr) {
   __shared__ SweepSmem sm[4];
+  constexpr bool STAGED = (MODE == 1 || MODE == 5) && kStagedAppend;
+  __shared__ int32_t stage[STAGED ? 4 * kStageWords : 1];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = g < n_ctr;
   // MODE 3: CSR row; MODE 1 / 5: SELL-32x4 column, entry k at dst[128 (k / 4) + k % 4]
@@ -200,7 +202,8 @@ __global__ void __launch_bounds__(128, 8) sweep_cell_kernel(
   int64_t ub = 0;
   // MODE 4 / 5: the slice's member masks (see near_sweep.cuh)
   unsigned* mk = ((MODE == 4 || MODE == 5) && (g >> 5) * 32 < n_ctr) ? mask + mptr[g >> 5] : nullptr;
-  sweep_warp<MODE>(in, sm[threadIdx.x >> 5], g, dst, INT_MAX, k, ub, mk);
+  sweep_warp<MODE, STAGED>(in, sm[threadIdx.x >> 5], g, dst, INT_MAX, k, ub, mk,
+                           STAGED ? stage + (threadIdx.x >> 5) * kStageWords : nullptr);
   if ((MODE == 0 || MODE == 4) && valid) cnt[g] = k;
   if ((MODE == 1 || MODE == 5) && valid && cnt) cnt[g] = k;
   if (MODE == 2 && (threadIdx.x & 31) == 0 && (g >> 5) * 32 < n_ctr)

@@ -179,6 +179,26 @@ constexpr unsigned kWalkAbove = TSQBX_WALK_ABOVE;
 #define TSQBX_INT4_STORES 1
 #endif
 constexpr bool kInt4Stores = TSQBX_INT4_STORES != 0;
+// SELL fill, dense groups: append row by row (every lane stores its own
+// candidate for the row in turn, empty rows skipped) instead of lane by lane
+#ifndef TSQBX_ROW_APPEND
+#define TSQBX_ROW_APPEND 0
+#endif
+constexpr bool kRowAppend = TSQBX_ROW_APPEND != 0;
+// SELL fill: members staged per lane in shared memory, 16 candidates at a
+// time with branch-free stores (a dense 32-candidate group costs ~190
+// instructions instead of ~770 for the register shift-register walk), whole
+// blocks flushed with 16-byte stores
+#ifndef TSQBX_STAGED_APPEND
+#define TSQBX_STAGED_APPEND 1
+#endif
+constexpr bool kStagedAppend = TSQBX_STAGED_APPEND != 0;
+constexpr int kStagePos = 20;                 // 3 pending + 16 new + 1 scratch slot
+constexpr int kStageWords = kStagePos * 32;
+#ifndef TSQBX_STAGE_ABOVE
+#define TSQBX_STAGE_ABOVE 12
+#endif
+constexpr unsigned kStageAbove = TSQBX_STAGE_ABOVE;
 // locate and L1-prefetch the next tile's candidates before testing this one
 #ifndef TSQBX_SWEEP_PREFETCH
 #define TSQBX_SWEEP_PREFETCH 1
@@ -222,10 +242,14 @@ struct SweepSmem {
 // 3: CSR row, dst[k]) up to row_cap entries (a multiple of 4); k_out is the
 // member count (> row_cap: the caller's buffer overflowed).  MODE 0 counts;
 // MODE 2 returns in ub_out the warp's bound (the largest candidate count).
-template <int MODE>
+// STAGED (SELL fills): `stage` is a per-warp shared-memory buffer of
+// kStageWords ints; a lane's members collect there ([position][lane], so a
+// lane's accesses never leave its bank) and go out as whole 16-byte blocks.
+template <int MODE, bool STAGED = false>
 __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int64_t g,
                                            int32_t* dst, int row_cap, int& k_out,
-                                           int64_t& ub_out, unsigned* mask = nullptr) {
+                                           int64_t& ub_out, unsigned* mask = nullptr,
+                                           int32_t* stage = nullptr) {
   const double* __restrict__ ctr = in.ctr;
   const double* __restrict__ rad = in.rad;
   const int64_t n_ctr = in.n_ctr;
@@ -276,6 +300,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
   auto run_cells = [&](int ncell, bool mine, double ox, double oy, double oz, double A,
                        unsigned* mk) {
     const bool from_mask = MODE == 5 && mk != nullptr;
+    const bool mine_all = __all_sync(0xffffffffu, mine);
     // fp32 prefilter in dot-product form: with s' = s - o, c' = c - o (every
     // coordinate |.| <= A) a candidate is a member iff
     //   f = s'.c' - |s'|^2 / 2  >=  K = (|c'|^2 - rad^2) / 2,
@@ -426,7 +451,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
             // (every lane stores its own) beats a per-lane loop that runs as
             // long as the busiest lane
             auto put = [&](int j) {
-              if (!SELLF || !kInt4Stores) {
+              if (!SELLF || !kInt4Stores || kRowAppend) {
                 if (k < row_cap) dst[MODE == 3 ? k : ((k >> 2) << 7) | (k & 3)] = j;
               } else {
                 // SELL: the row's current block as a 4-entry shift register,
@@ -441,7 +466,104 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
               ++k;
             };
             // (only the lanes testing this list are active here: per-cell mode)
-            if (__reduce_max_sync(__activemask(), (unsigned)__popc(bits)) >= kWalkAbove) {
+            if (SELLF && STAGED) {
+              // the row's pending entries (k & 3 of them) sit at positions
+              // 0 .. (k & 3) - 1 of this lane's stage column
+              int32_t* const col = stage + lane;
+              auto flush_block = [&](int b) {          // stage positions 4b .. 4b + 3 -> row block
+                const int blk = (k >> 2) + b;
+                int4 v;
+                v.x = col[(4 * b) << 5];
+                v.y = col[(4 * b + 1) << 5];
+                v.z = col[(4 * b + 2) << 5];
+                v.w = col[(4 * b + 3) << 5];
+                if (4 * blk + 3 < row_cap) *reinterpret_cast<int4*>(dst + (blk << 7)) = v;
+              };
+              const unsigned am = __activemask();
+              if (__reduce_max_sync(am, (unsigned)__popc(bits)) >= kStageAbove) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const unsigned hb = h == 0 ? bits >> 16 : bits & 0xffffu;   // candidate u: bit 15 - u
+                  if (!__any_sync(am, hb != 0u)) continue;
+                  const int r = k & 3;
+                  int32_t* p = col + (r << 5);
+                  const int4* tq = reinterpret_cast<const int4*>(&sm.tid[t0 + 16 * h]);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const int4 j4 = tq[q];
+                    // unconditional store, conditional advance: a rejected
+                    // candidate is overwritten by the next one
+                    *p = j4.x;
+                    p += (hb & (0x8000u >> (4 * q))) ? 32 : 0;
+                    *p = j4.y;
+                    p += (hb & (0x4000u >> (4 * q))) ? 32 : 0;
+                    *p = j4.z;
+                    p += (hb & (0x2000u >> (4 * q))) ? 32 : 0;
+                    *p = j4.w;
+                    p += (hb & (0x1000u >> (4 * q))) ? 32 : 0;
+                  }
+                  const int n = r + __popc(hb);
+                  const int nb = n >> 2;
+                  const int top = (int)__reduce_max_sync(am, (unsigned)nb);
+                  for (int b = 0; b < top; ++b)
+                    if (b < nb) flush_block(b);
+                  if (nb > 0) {                        // the open block moves to the front
+                    const int32_t* tail = col + ((4 * nb) << 5);
+                    const int a0 = tail[0], a1 = tail[32], a2 = tail[64];
+                    col[0] = a0;
+                    col[32] = a1;
+                    col[64] = a2;
+                  }
+                  k = k - r + n;
+                }
+              } else {
+                while (bits) {
+                  const int u = __clz(bits);
+                  bits &= ~(0x80000000u >> u);
+                  col[(k & 3) << 5] = sm.tid[t0 + u];
+                  if ((k & 3) == 3) {
+                    k -= 3;
+                    flush_block(0);
+                    k += 3;
+                  }
+                  ++k;
+                }
+              }
+            } else if (SELLF && kRowAppend && mine_all) {
+              // Whole warp testing one list (union mode, 32 valid rows).  A dense
+              // group is appended row by row: the row's mask and length are
+              // broadcast, lane u stores candidate u (still in its register from
+              // the staging) at the row's next free slot plus the rank of bit u;
+              // rows without a member in the group are skipped, which is most of
+              // them -- a row's members fill a few of the warp's groups.  Sparse
+              // groups (few members per lane) keep the per-lane loop.
+              const unsigned rows_ne = __ballot_sync(0xffffffffu, bits != 0u);
+              const unsigned busiest = __reduce_max_sync(0xffffffffu, (unsigned)__popc(bits));
+              if (5u * (unsigned)__popc(rows_ne) < 4u * busiest) {
+                int my = jc[0];
+#pragma unroll
+                for (int r = 1; r < kTile / 32; ++r)
+                  if (t0 == 32 * r) my = jc[r];
+                int32_t* const slice = dst - 4 * lane;
+                unsigned rows = rows_ne;
+                while (rows) {
+                  const int r = __ffs(rows) - 1;
+                  rows &= rows - 1;
+                  const unsigned b = __shfl_sync(0xffffffffu, bits, r);
+                  const int kr = __shfl_sync(0xffffffffu, k, r);
+                  const int kk = kr + __popc((b >> 1) >> (31 - lane));   // members before bit 31 - lane
+                  if ((int)(b << lane) < 0 && kk < row_cap)
+                    slice[4 * r + (((kk >> 2) << 7) | (kk & 3))] = my;
+                }
+                k += __popc(bits);
+              } else {
+                while (bits) {
+                  const int u = __clz(bits);
+                  bits &= ~(0x80000000u >> u);
+                  put(sm.tid[t0 + u]);
+                }
+              }
+            } else if (__reduce_max_sync(__activemask(), (unsigned)__popc(bits)) >= kWalkAbove) {
 #pragma unroll 4
               for (int u = 0; u < 32; ++u) {
                 const int j = sm.tid[t0 + u];
@@ -592,7 +714,12 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
       }
     }
   }
-  if (SELLF && kInt4Stores && valid && (k & 3) && k < row_cap) {   // the last, partial block
+  if (SELLF && STAGED) {
+    if (valid && (k & 3) && (k | 3) < row_cap) {        // the last, partial block (tail slots unread)
+      const int32_t* col = stage + lane;
+      *reinterpret_cast<int4*>(dst + ((k >> 2) << 7)) = make_int4(col[0], col[32], col[64], 0);
+    }
+  } else if (SELLF && kInt4Stores && !kRowAppend && valid && (k & 3) && k < row_cap) {   // the last, partial block
     const int r = k & 3;                                // entries pending in pend's tail
     int4 blk = pend;
     if (r == 1) blk.x = pend.w;

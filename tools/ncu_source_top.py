@@ -22,9 +22,14 @@ for r in rows:
         cur["lines"].append(r)
     elif cur is not None and len(r) > 8 and r[0] == "Line No":
         cur["hdr"] = r
+# a kernel has one section per source file it inlines code from: merge them
+merged = {}
 for sec in sections:
     if pat not in sec["name"] or not sec["lines"]:
         continue
+    m = merged.setdefault(sec["name"], {"name": sec["name"], "lines": [], "hdr": sec["hdr"]})
+    m["lines"] += sec["lines"]
+for sec in merged.values():
     h = sec["hdr"]
     ie, sm = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
     tot_i = sum(float(r[ie] or 0) for r in sec["lines"])
