@@ -168,17 +168,6 @@ __device__ __forceinline__ bool member(const double4 s, double cx, double cy, do
 // measured equal on dense lists, 9 % faster on the literal preset
 constexpr int kTile = 128;
 constexpr int kMaxCells = 128;   // cells one union pass stages (non-empty ones)
-// Single-level grids (more than kMultiLevelMaxSources sources): cells a union
-// region may cover.  They are looked up, and around a surface most are empty;
-// more than kMaxCells non-empty ones fall back to the per-cell passes.  C5
-// literal: the large spheres' regions cover ~340 cells of which ~50 hold
-// sources -- one union pass instead of ~16 per-cell passes (build 7.6 -> 6.9
-// ms).  With several levels the next coarser level is the cheaper answer
-// (measured: C4 dense 2.45 -> 2.98 ms when they look up 512 cells too).
-#ifndef TSQBX_MAX_LOOK
-#define TSQBX_MAX_LOOK 512
-#endif
-constexpr int kMaxLook = TSQBX_MAX_LOOK;
 // fill: members of the busiest lane in a 32-candidate group from which the
 // append walks all 32 candidates instead of each lane's own members
 #ifndef TSQBX_WALK_ABOVE
@@ -638,7 +627,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
       const unsigned long long n = ((fhi[0] >> sh) - (flo[0] >> sh) + 1) *
                                    ((fhi[1] >> sh) - (flo[1] >> sh) + 1) *
                                    ((fhi[2] >> sh) - (flo[2] >> sh) + 1);
-      if (n <= (unsigned long long)(top == 0 ? kMaxLook : kMaxCells)) {
+      if (n <= (unsigned long long)kMaxCells) {
         lw = L;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -649,7 +638,6 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
       }
     }
   }
-  bool per_cell = lw < 0;
   if (lw >= 0) {
     // the region's cells (x-major order), non-empty ones compacted in order
     const unsigned long long ex = chi[0] - clo[0] + 1, ey = chi[1] - clo[1] + 1,
@@ -657,9 +645,8 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
     const int ncell = (int)(ex * ey * ez);
     int n_ne = 0;
     int64_t mine_sz = 0;
-#pragma unroll 4
-    for (int slot = 0; slot < kMaxLook / 32; ++slot) {
-      if (32 * slot >= ncell) break;
+#pragma unroll
+    for (int slot = 0; slot < kMaxCells / 32; ++slot) {
       const int c = lane + 32 * slot;
       int st = 0, en = 0;
       if (c < ncell) {
@@ -670,18 +657,14 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
       const unsigned ne = __ballot_sync(0xffffffffu, en > st);
       const int at = n_ne + __popc(ne & ((1u << lane) - 1u));
       if (en > st) {
-        if (at < kMaxCells) {
-          sm.cell_st[at] = st;
-          sm.cell_en[at] = en;
-        }
+        sm.cell_st[at] = st;
+        sm.cell_en[at] = en;
         mine_sz += en - st;
       }
       n_ne += __popc(ne);
     }
     __syncwarp();
-    if (n_ne > kMaxCells) {
-      per_cell = true;                   // more non-empty cells than a pass stages
-    } else if (MODE == 2) {
+    if (MODE == 2) {
       for (int off = 16; off > 0; off >>= 1) mine_sz += __shfl_xor_sync(0xffffffffu, mine_sz, off);
       ub = mine_sz;
     } else if (n_ne > 0) {
@@ -694,8 +677,7 @@ __device__ __forceinline__ void sweep_warp(const SweepIn& in, SweepSmem& sm, int
       const double A = fmax(bhi[0] - blo[0], fmax(bhi[1] - blo[1], bhi[2] - blo[2])) + rb + 2.0 * cs;
       run_cells(n_ne, valid, ox, oy, oz, A, mask);
     }
-  }
-  if (per_cell && any_valid) {
+  } else if (any_valid) {
     // per distinct cell of the warp: its 27 neighbours, only that cell's lanes test
     // one head per distinct (cell, level): lanes of one cell need not be
     // adjacent when their levels differ
