@@ -3,6 +3,8 @@
 // eval_helmholtz.cu) and the fused build+evaluate kernel (fused.cu).
 #pragma once
 
+#include <type_traits>
+
 #include "eval_kernels.cuh"
 
 // 1: the SELL S kernel sums over orders by Clenshaw on the Hankel recurrence
@@ -154,6 +156,30 @@ __device__ __forceinline__ void helmholtz_sell_row(const EvalParams& a, int64_t 
       }
       ar[q] = ai[q] = 0.0;
     }
+    // A single dependent DFMA chain fills the FP64 pipe of an SM to 66 % at
+    // most (tools/micro/dp_chain.cu), so the chains of one source -- 1/R, the
+    // two Horner chains of sin/cos, the Legendre recurrence, the Clenshaw
+    // recurrence -- should sit in ONE basic block for the scheduler to
+    // interleave; hankel01's choice of series branches per source and cuts the
+    // block in three.  kStruct picks how the choice is made (measured per
+    // kernel family, C5/C3 dense and literal):
+    //   2 (one target, long rows): the row's loop exists once per series
+    //     (LOOP_ 1 narrow, 2 wide, 0 per-source choice with the library
+    //     fallback), picked outside the loop from the k R hint, so a source's
+    //     whole arithmetic is one block (C5 dense 12.31 -> 11.86 ms).  The hint
+    //     is checked per row on the integer pipe (largest R^2 as its bit
+    //     pattern); a row that violates it is recomputed on the generic loop.
+    //   1 (two targets): one warp-uniform branch per source picks the series
+    //     and everything after it is one block (C3 dense 0.506 -> 0.497 ms).
+    //   0 (one target, short rows): hankel01 as it is -- the copies of the
+    //     loop cost the short rows more than the interleaving gives (C5
+    //     literal 0.619 ms against 0.647 / 0.680 ms).
+    constexpr int kStruct = NT == 1 ? (CFR ? 2 : 0) : 1;
+    long long rmax = 0;
+    auto run = [&](auto loop_tag) {
+    constexpr int LOOP_ = decltype(loop_tag)::value;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) ar[q] = ai[q] = 0.0;
     SellStream<> ss(a, soff >= 0 ? soff : a.sell_ptr[g >> 5], g, len, false, ring, true);
     while (ss.more()) {
       double4 q4;
@@ -163,8 +189,21 @@ __device__ __forceinline__ void helmholtz_sell_row(const EvalParams& a, int64_t 
       const double R2 = fma(dz, dz, fma(dy, dy, dx * dx));
       const double iR = rsqrt_fast(R2);
       const double invx = iR * invk;
+      auto rest = [&](auto series_tag) {
+      constexpr int MODE_ = decltype(series_tag)::value;
       double hmr, hmi, hcr, hci;                 // h_{n-1}, h_n
-      hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci, a.series);
+      if constexpr (MODE_ == 0) {
+        // (kStruct 2 gets here without a hint or after the hint failed: series 0)
+        hankel01(a.sc, k2 * R2, k * (R2 * iR), invx, hmr, hmi, hcr, hci,
+                 kStruct == 2 ? 0 : a.series);
+      } else {
+        double sinc, cs;
+        sinc_cos_series<MODE_ == 2>(a.sc, k2 * R2, sinc, cs);
+        hmr = sinc;
+        hmi = -cs * invx;
+        hcr = fma(hmr, invx, hmi);
+        hci = fma(hmi, invx, -hmr);
+      }
       double cg[NT], sr[NT], si[NT];
       if constexpr (kClenshaw) {
         // sum_n a_n h_n, a_n = c_n P_n(cos g) real, by Clenshaw over the Hankel
@@ -251,7 +290,32 @@ __device__ __forceinline__ void helmholtz_sell_row(const EvalParams& a, int64_t 
         ar[q] = fma(q4.w, sr[q], fma(-wim, si[q], ar[q]));
         ai[q] = fma(q4.w, si[q], fma(wim, sr[q], ai[q]));
       }
+      };
+      if constexpr (kStruct == 1) {
+        // the series picked per source by a warp-uniform branch; everything
+        // after it is one basic block
+        if (a.series == 1) rest(std::integral_constant<int, 1>{});
+        else if (a.series == 2 && __all_sync(__activemask(), k2 * R2 <= kWideX2))
+          rest(std::integral_constant<int, 2>{});
+        else rest(std::integral_constant<int, 0>{});
+      } else {
+        rest(loop_tag);
+      }
       if (VAL) rmin = min(rmin, __double_as_longlong(R2));
+      if (kStruct == 2 && LOOP_ != 0) rmax = max(rmax, __double_as_longlong(R2));
+    }
+    };
+    if constexpr (kStruct == 2) {
+      // (an explicit fourth copy for the recomputation: folding it into a loop
+      // over `series` costs 9 % on C5 dense)
+      if (a.series == 1) run(std::integral_constant<int, 1>{});
+      else if (a.series == 2) run(std::integral_constant<int, 2>{});
+      else run(std::integral_constant<int, 0>{});
+      if (a.series != 0 &&
+          k2 * __longlong_as_double(rmax) > (a.series == 1 ? kSmallX2 : kWideX2) * (1.0 + 1e-9))
+        run(std::integral_constant<int, 0>{});   // the k R hint does not hold for this row
+    } else {
+      run(std::integral_constant<int, 0>{});
     }
     const double pk = k * kInvFourPi;
 #pragma unroll

@@ -21,7 +21,9 @@ import pytest
 import torch
 
 import oracle
-from paper_1811_01110_b200 import TsqbxProblem, _lib, build_near_lists, configs
+from paper_1811_01110_b200 import (KernelSpec, TsConfig, TsqbxProblem, _lib, build_near_lists,
+                                   configs)
+from paper_1811_01110_b200.kernels import Equation
 
 pytestmark = pytest.mark.gpu
 
@@ -220,3 +222,30 @@ def test_reference_named_p2p_entry_points(eq, variant):
     print(f"\ntsqbx_p2p_{eq} variant {variant}: normwise err {e:.3e}")
     assert e <= (LAP_TOL if eq == "laplace" else HELM_TOL)
     assert int(err.item()) == _lib.ERR_KEY_NONE
+
+
+@pytest.mark.parametrize("claimed", ["narrow", "wide"])
+def test_helmholtz_kr_hint_violated_is_recomputed(claimed):
+    """The one-target long-row Helmholtz kernel picks its e^{ikR} series outside
+    the row loop from the k R hint (FLAG_KR_NARROW / FLAG_KR_WIDE) and checks the
+    hint per row (largest R^2 on the integer pipe): rows that violate it are
+    recomputed on the generic path.  A near list that claims a far too small
+    radius must still give the oracle's potentials."""
+    import math
+    case = configs.make_case("c5", "dense", n=8192, spheres=2)
+    k = 60.0                     # k R up to ~2.4: beyond both series' intervals on many rows
+    cfg = TsConfig(KernelSpec(equation=Equation.HELMHOLTZ, helmholtz_k=k), case.cfg.p_qbx)
+    near = build_near_lists(case.centers, case.sources, case.near_radii)
+    true_kr = k * near.max_radius
+    assert true_kr > math.pi / 2 and near.mean_len >= 48
+    near.max_radius = (0.5 if claimed == "narrow" else 1.5) / k      # k R "<= pi/4" / "<= pi/2"
+    prob = TsqbxProblem(cfg, case.sources, case.weights, case.centers, case.targets, near,
+                        tgt_ptr=case.tgt_ptr)
+    assert prob.prep.kr_flag != 0 and prob.prep.tuni == 1
+    got = prob.evaluate(validate=False).cpu().numpy()
+    uptr, uidx = near.to_user_csr()
+    ref = oracle.ts_batch("helmholtz", 0, k, cfg.p_qbx, case.sources, case.weights, case.centers,
+                          uptr, uidx, case.targets, case.tgt_ptr)
+    err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+    print(f"kr hint {claimed} violated (true k R {true_kr:.2f}): normwise {err:.2e}")
+    assert err <= 1e-10

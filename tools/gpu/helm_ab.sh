@@ -1,9 +1,10 @@
-for v in default helm3 onet; do
-  unset GIGAQBX_LIB_PATH GIGAQBX_ONE_TARGET
-  if [ $v = helm3 ]; then export GIGAQBX_LIB_PATH=paper_1811_01110_b200/_lib/variants/helm3.so; fi
-  if [ $v = onet ]; then export GIGAQBX_ONE_TARGET=1; fi
-  for c in "c3 literal" "c3 dense" "c5 literal" "c2 literal"; do
+# Helmholtz S SELL kernel A/B over library variants: parity, then timings of the Helmholtz presets
+timeout 900 python -m pytest tests/test_gpu_timed_path.py tests/test_gpu_parity.py tests/test_gpu_fused.py -x -q -k "c5 or c3 or helm or Helm or fused" > gpurun_out/t_helm.log 2>&1; echo rc=$? >> gpurun_out/t_helm.log
+for v in default base; do
+  unset GIGAQBX_LIB_PATH
+  [ $v != default ] && export GIGAQBX_LIB_PATH=$PWD/paper_1811_01110_b200/_lib/variants/$v.so
+  for c in "c5 dense" "c5 literal" "c3 dense" "c3 literal"; do
     set -- $c
-    echo -n "$v: "; timeout 300 python tools/profile_case.py --case $1 --preset $2 --reps 3 2>&1 | tail -1
+    echo -n "$v "; timeout 300 python tools/profile_case.py --case $1 --preset $2 --reps 5 2>&1 | tail -1
   done
-done > gpurun_out/helm_ab.log 2>&1
+done > gpurun_out/helm_time.log 2>&1
