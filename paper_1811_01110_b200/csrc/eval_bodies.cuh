@@ -330,118 +330,4 @@ __device__ __forceinline__ void helmholtz_sell_row(const EvalParams& a, int64_t 
 }
 #undef CF
 
-// Helmholtz S, one target per center, long rows: TWO sources per iteration in
-// lockstep.  A source's arithmetic is three serial DP chains one after the
-// other (1/R and e^{ikR}, the Legendre recurrence upward, Clenshaw downward),
-// and with 128 registers per thread only four warps share a scheduler -- not
-// enough independent DFMAs to cover the pipe's latency (ncu: FP64 pipe 70 %,
-// top stall `wait`).  Two sources give every chain an independent twin; the
-// target coefficients move to shared memory (read once per order and source
-// pair) to pay for the second source's registers.  An odd tail repeats the
-// last source with weight zero.
-template <int P, bool VAL, int UNI>
-__device__ __forceinline__ void helmholtz_sell_row2(const EvalParams& a, int64_t g, int len,
-                                                    double* cfs, int4* ring) {
-  auto cf = [&](int n) -> double& { return cfs[n * kSellBlock + threadIdx.x]; };
-  const double cx = a.ctr[3 * g], cy = a.ctr[3 * g + 1], cz = a.ctr[3 * g + 2];
-  const int64_t t0 = UNI > 0 ? a.tbase + g * UNI : a.tptr[g], t1 = UNI > 0 ? t0 + UNI : a.tptr[g + 1];
-  const double k = a.k, k2 = a.k * a.k, invk = 1.0 / a.k;
-  for (int64_t tb = t0; tb < t1; ++tb) {
-    long long rmin = 0x7ff0000000000000ll;
-    const int64_t slot = out_slot(a, tb);
-    const double ux = a.tgt[3 * tb] - cx, uy = a.tgt[3 * tb + 1] - cy, uz = a.tgt[3 * tb + 2] - cz;
-    const double r2 = fma(uz, uz, fma(uy, uy, ux * ux));
-    const double ir = r2 > 0.0 ? rsqrt(r2) : 0.0;        // r = 0: cos g irrelevant
-    const double tx = ux * ir, ty = uy * ir, tz = uz * ir;
-    {
-      double jn[P + 1];
-      const double rr = r2 * ir;                         // |t - c|
-      if (rr > 0.0) {
-        sph_j_reg<P + 1>(k * rr, jn);
-      } else {
-#pragma unroll
-        for (int n = 0; n <= P; ++n) jn[n] = n == 0 ? 1.0 : 0.0;   // j_n(0), _core.pyx:357
-      }
-#pragma unroll
-      for (int n = 0; n <= P; ++n) cf(n) = c_leg.hsc[n] * jn[n];
-    }
-    double ar = 0.0, ai = 0.0;
-    SellStream<> ss(a, a.sell_ptr[g >> 5], g, len, false, ring, true);
-    while (ss.more()) {
-      double4 q4[2];
-      double wim[2];
-      ss.next(q4[0], wim[0]);
-      if (ss.more()) {
-        ss.next(q4[1], wim[1]);
-      } else {
-        q4[1] = q4[0];
-        q4[1].w = 0.0;
-        wim[1] = 0.0;
-      }
-      double dx[2], dy[2], dz[2], invx[2], cg[2], hmr[2], hmi[2], hcr[2], hci[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        dx[s] = q4[s].x - cx;
-        dy[s] = q4[s].y - cy;
-        dz[s] = q4[s].z - cz;
-        const double R2 = fma(dz[s], dz[s], fma(dy[s], dy[s], dx[s] * dx[s]));
-        const double iR = rsqrt_fast(R2);
-        invx[s] = iR * invk;
-        hankel01(a.sc, k2 * R2, k * (R2 * iR), invx[s], hmr[s], hmi[s], hcr[s], hci[s], a.series);
-        cg[s] = fma(dz[s], tz, fma(dy[s], ty, dx[s] * tx)) * iR;
-        if (VAL) rmin = min(rmin, __double_as_longlong(R2));
-      }
-      // scaled Legendre terms a'_n = c_n kappa'_n P_n(cos g) upward, both sources
-      double ap[2][P + 1];
-      if constexpr (P >= 1) {
-        double um[2] = {1.0, 1.0}, uc[2] = {cg[0], cg[1]};
-        {
-          const double c1 = cf(1);
-          ap[0][1] = c1 * uc[0];
-          ap[1][1] = c1 * uc[1];
-        }
-#pragma unroll
-        for (int n = 1; n < P; ++n) {
-          const double cn = cf(n + 1);
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const double un = fma(c_leg.alpha[n] * cg[s], uc[s], -um[s]);
-            um[s] = uc[s];
-            uc[s] = un;
-            ap[s][n + 1] = cn * un;
-          }
-        }
-      }
-      // Clenshaw over the Hankel recurrence downward (see helmholtz_sell_row)
-      const double c0 = cf(0);
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        double g1 = 0.0, g2 = 0.0;
-        if constexpr (P >= 1) {
-          g1 = ap[s][P];
-          if constexpr (P >= 2) {
-            g2 = g1;
-            g1 = fma(invx[s], g2, ap[s][P - 1]);
-          }
-#pragma unroll
-          for (int n = P - 2; n >= 1; --n) {
-            const double gg = fma(invx[s], g1, fma(-c_leg.gam[n], g2, ap[s][n]));
-            g2 = g1;
-            g1 = gg;
-          }
-        }
-        const double t0c = P >= 2 ? fma(-1.0 / 3.0, g2, c0) : c0;
-        const double sr = fma(hcr[s], g1, hmr[s] * t0c);
-        const double si = fma(hci[s], g1, hmi[s] * t0c);
-        ar = fma(q4[s].w, sr, fma(-wim[s], si, ar));
-        ai = fma(q4[s].w, si, fma(wim[s], sr, ai));
-      }
-    }
-    const double pk = k * kInvFourPi;
-    a.out[slot] = make_double2(-ai * pk, ar * pk);      // (ik/4pi) acc
-    if (VAL && (!isfinite(ar) || !isfinite(ai) || r2 > kSepScreen * __longlong_as_double(rmin)))
-      flag_suspect(a.err);
-  }
-}
-
 }  // namespace tsqbx

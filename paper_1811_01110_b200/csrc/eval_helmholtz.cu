@@ -113,28 +113,13 @@ __global__ void __launch_bounds__(256) helmholtz_s_kernel(const EvalParams a) {
 // with 2 CTAs per SM instead of shared memory with 3 -- long rows (dense
 // presets: C5 dense -2 %), where the extra warps of the 3-CTA build only help
 // short rows hide their per-row latency (C5 literal +14 %)
-// CFR = 2 (one target per center, long rows): two sources per iteration in
-// lockstep, coefficients in shared memory (helmholtz_sell_row2)
-// measured slower (C5 dense 14.0 vs 12.3 ms: the second source's registers
-// and the shared-memory coefficient loads cost more than the extra
-// independent chains give) and compiled out
-#ifndef TSQBX_HELM_DUAL
-#define TSQBX_HELM_DUAL 0
-#endif
-#ifndef TSQBX_HELM_DUAL_MINB
-#define TSQBX_HELM_DUAL_MINB 2
-#endif
 template <int P, int NT, bool VAL, int UNI, int CFR = 0>
-__global__ void __launch_bounds__(kSellBlock, NT == 1 ? (CFR == 2 ? TSQBX_HELM_DUAL_MINB : CFR ? 2 : TSQBX_HELM_MINB1) : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
+__global__ void __launch_bounds__(kSellBlock, NT == 1 ? (CFR ? 2 : TSQBX_HELM_MINB1) : TSQBX_HELM_MINB) helmholtz_sell_kernel(const EvalParams a) {
   extern __shared__ double cfs[];
   __shared__ int4 ring[kSlots * kSellBlock];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < a.n_ctr) {
-    if constexpr (CFR == 2 && NT == 1)
-      helmholtz_sell_row2<P, VAL, UNI>(a, g, (int)(a.nptr[g + 1] - a.nptr[g]), cfs, ring);
-    else
-      helmholtz_sell_row<P, NT, VAL, UNI, CFR>(a, g, -1, (int)(a.nptr[g + 1] - a.nptr[g]), cfs, ring);
-  }
+  if (g < a.n_ctr)
+    helmholtz_sell_row<P, NT, VAL, UNI, CFR>(a, g, -1, (int)(a.nptr[g + 1] - a.nptr[g]), cfs, ring);
 }
 
 template <template <int> class F, int... Ps>
@@ -156,15 +141,7 @@ struct HelmholtzLaunch {
       const int grid = (int)((n_ctr + kSellBlock - 1) / kSellBlock);
       bool done = false;
       if constexpr (NT == 1) {
-#if TSQBX_HELM_DUAL
-        if (a.long_rows && P >= 2) {
-          const int smem = (P + 1) * kSellBlock * (int)sizeof(double);
-          (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT, 2>
-                        : helmholtz_sell_kernel<P, NT, VAL, 0, 2>)<<<grid, kSellBlock, smem, st>>>(a);
-          done = true;
-        }
-#endif
-        if (!done && a.long_rows) {
+        if (a.long_rows) {
           (a.tuni == NT ? helmholtz_sell_kernel<P, NT, VAL, NT, 1>
                         : helmholtz_sell_kernel<P, NT, VAL, 0, 1>)<<<grid, kSellBlock, 0, st>>>(a);
           done = true;
